@@ -1,0 +1,170 @@
+/* =====================================================================================
+ * rtm.h — C ABI of the B200-native RTM 3D-model time step (arxiv 1310.8232).
+ *
+ * The operation (§2 "3D Stencil Computations": finite differences, "10th
+ * order in space and 2nd order in time", a stencil that "refers to five points (cells)
+ * in each direction for each dimension"; Algorithm 1 line "forall points:
+ * calculate 3D model", 99% of RTM time):
+ *
+ *     u^{n+1}(p) = 2 u^n(p) - u^{n-1}(p) + C(p) * sum_{axis} sum_{o=-5..5} c_|o| u^n(p + o e_axis)
+ *     C(p)       = fp32( (double(v(p)) * double(dt) / double(dx))^2 )        (a1)
+ *     u^{n+1}(p_s) += w_s[n]   for each registered source s, in registration order (a3)
+ *
+ * with a 5-cell zero (Dirichlet) halo around the nx*ny*nz interior.  Coefficients, halo,
+ * source form and precision are the readings R1-R16 of DESIGN.md (the paper is silent on
+ * them; BASELINE.json configs[0] fixes c0..c5).  Arithmetic is fp32 on the GPU.
+ *
+ * Layout: every host array is the unpadded interior, x fastest, then y, then z:
+ *     index(x, y, z) = (z * ny + y) * nx + x          (float32)
+ *
+ * Conventions
+ *  - Every int-returning call returns RTM_OK (0) or a negative RTM_E* code.  Nothing
+ *    throws or aborts across the ABI.  rtm_last_error() returns a thread-local message
+ *    naming the offending argument or the failing CUDA/NCCL call.
+ *  - Ownership: the caller owns every host (and user device) buffer it passes; the library
+ *    copies what it needs before returning.  The context owns its device memory, streams,
+ *    events, graphs and NCCL communicator; rtm_destroy releases them.
+ *  - A context is used by one host thread at a time ("confined to one worker").
+ *  - No CPU fallback: every step of the path runs in the library's sm_100a kernels.  A
+ *    context cannot be created without a CUDA device (rtm_create returns NULL, RTM_ECUDA).
+ * ===================================================================================== */
+#ifndef RTM_H_
+#define RTM_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rtm_ctx rtm_ctx; /* opaque; owned by the library */
+
+enum {
+    RTM_OK = 0,
+    RTM_EINVAL = -1, /* invalid argument (sizes, non-finite values, coordinates, ids)       */
+    RTM_ECFL = -2,   /* max(v)*dt/dx exceeds nu_crit(coeffs) = 2/sqrt(3*S_max)              */
+    RTM_ENOMEM = -3, /* device or host allocation failed                                    */
+    RTM_ECUDA = -4,  /* a CUDA runtime/driver call or kernel failed                          */
+    RTM_ENCCL = -5,  /* an NCCL call failed                                                  */
+    RTM_ESTATE = -6  /* call not valid in this state (e.g. rtm_step before rtm_set_velocity) */
+};
+
+#define RTM_MAX_SOURCES 64
+
+/* ---- north-star entry points (BASELINE.json north_star) ------------------------------ */
+
+/* Create a single-GPU context on the current CUDA device for an nx*ny*nz interior grid.
+ * dx > 0 (m), dt > 0 (s) finite; coeffs[0..5] = c0..c5 finite, with S_max > 0 (a valid
+ * negative-definite 2nd difference).  Allocates u, u_prev (each nx*ny*(nz+10) floats:
+ * 5 explicit zero z-halo planes per side) and C (nx*ny*nz floats), zero-initialised.
+ * Returns NULL on error (see rtm_last_error()). */
+rtm_ctx* rtm_create(int nx, int ny, int nz, float dx, float dt, const float coeffs[6]);
+
+/* Host velocity v (m/s), nx*ny*nz_local floats (the whole grid, or this rank's slab for
+ * rtm_create_dist).  Copied to the device, where a kernel computes C(p) in fp64 and rounds
+ * once to fp32 (a1).  Every v must be finite and > 0 (RTM_EINVAL) and
+ * max(v)*dt/dx <= nu_crit (RTM_ECFL, nu_crit = 5/sqrt(128) for the configs' coefficients).
+ * On error no velocity is installed. */
+int rtm_set_velocity(rtm_ctx* ctx, const float* v);
+
+/* Register a point source at GLOBAL interior coordinates (ix, iy, iz).  samples[n]
+ * (nsamples >= 0 floats, host, copied) is added to u^{n+1}(p_s) right after the stencil of
+ * step n (n counted from the last rtm_reset/rtm_set_fields), for n < nsamples (a3).
+ * Sources at the same point add in registration order.  At most RTM_MAX_SOURCES.
+ * Coordinates outside the interior or a non-finite sample -> RTM_EINVAL.  In a distributed
+ * context every rank registers every source; a rank keeps the ones it owns. */
+int rtm_inject_source(rtm_ctx* ctx, int ix, int iy, int iz, const float* samples, int nsamples);
+
+/* Advance nsteps >= 0 time steps.  Returns after device completion (surfaces asynchronous
+ * errors).  RTM_ESTATE before rtm_set_velocity. */
+int rtm_step(rtm_ctx* ctx, int nsteps);
+
+/* Copy the current field u^n to host out (nx*ny*nz_local floats; the whole grid for
+ * multi-slab contexts, this rank's slab for distributed ones). */
+int rtm_read_field(rtm_ctx* ctx, float* out);
+
+void rtm_destroy(rtm_ctx* ctx);
+const char* rtm_last_error(void);
+
+/* ---- extensions (tests, bench, multi-GPU; not in the north-star list) ----------------- */
+
+/* Initial conditions / resume: u^0 = u, u^{-1} = u_prev (host, nx*ny*nz_local each; either
+ * may be NULL = zero).  Resets the step counter to 0. */
+int rtm_set_fields(rtm_ctx* ctx, const float* u, const float* u_prev);
+/* Read both time levels (u^n, u^{n-1}); either pointer may be NULL. */
+int rtm_read_fields(rtm_ctx* ctx, float* u, float* u_prev);
+/* u = u_prev = 0 and step = 0; keeps velocity, sources and tile choice. */
+int rtm_reset(rtm_ctx* ctx);
+/* Number of steps taken since the last reset / set_fields. */
+long long rtm_step_count(rtm_ctx* ctx);
+
+/* Device-resident variants (the bench's kernel-only leg): d_v / d_out are device pointers
+ * on the context's device (single-slab contexts only), same layout as the host versions.
+ * Enqueued on the context's stream; d_v must stay valid until the next synchronising call. */
+int rtm_set_velocity_device(rtm_ctx* ctx, const float* d_v);
+int rtm_read_field_device(rtm_ctx* ctx, float* d_out);
+
+/* Kernel variant ("tile", the GPU analogue of the paper's blocksize):
+ * -1 = automatic (default), 0 = naive one-thread-per-point kernel, 1..rtm_num_tiles()-1 =
+ * TMA-staged xy tiles.  Unknown id -> RTM_EINVAL.  Every variant computes bitwise-identical
+ * results (one per-point expression). */
+int rtm_set_tile(rtm_ctx* ctx, int tile_id);
+int rtm_get_tile(rtm_ctx* ctx);          /* the variant rtm_step will use (resolves -1) */
+int rtm_num_tiles(void);
+/* z-chunk length (planes) of a tiled work unit; 0 = automatic (minimises wave quantisation
+ * times chunk-halo re-reads). */
+int rtm_set_zchunk(rtm_ctx* ctx, int planes);
+const char* rtm_tile_name(int tile_id);  /* e.g. "tma64x16k10"; NULL for unknown ids */
+
+/* Run on the caller's CUDA stream (a cudaStream_t, e.g. torch.cuda.current_stream()); NULL
+ * restores the library's own stream.  Single-GPU or distributed (one slab per process)
+ * contexts only (RTM_EINVAL for multi-slab contexts). */
+int rtm_set_stream(rtm_ctx* ctx, void* cuda_stream);
+
+/* CUDA-event time of the last rtm_step call (ms). */
+float rtm_last_elapsed_ms(rtm_ctx* ctx);
+
+/* Per-launch stencil timing (bench roofline): when on, rtm_step records CUDA events around
+ * every stencil launch (and does not use CUDA graphs); rtm_kernel_stats returns the
+ * launches and summed device time (ms) since it was switched on / last read, then clears. */
+int rtm_set_profiling(rtm_ctx* ctx, int on);
+int rtm_kernel_stats(rtm_ctx* ctx, long long* launches, double* total_ms);
+/* Stencil launches issued by the library since creation (all kernels of the step). */
+long long rtm_launch_count(rtm_ctx* ctx);
+
+/* ---- z-slab decomposition -------------------------------------------- */
+
+/* One process, several slabs: the grid is split into nslabs z-slabs, slab r on CUDA device
+ * devices[r] (devices may repeat, e.g. all 0, to run the decomposition on one GPU).  Halos
+ * move by cudaMemcpyPeerAsync (copy engines) between slabs each step.  Host arrays are the
+ * whole grid.  Requires nz/nslabs >= 10 for every slab. */
+rtm_ctx* rtm_create_multi(int nx, int ny, int nz, float dx, float dt, const float coeffs[6],
+                          int nslabs, const int* devices);
+
+/* One process per GPU (torchrun): rank owns global planes [z0, z0+nzl) (rtm_slab_range).
+ * id = 128-byte NCCL unique id from rtm_get_unique_id() on rank 0, broadcast by the caller
+ * (torch.distributed).  Each step sends/receives the 5 boundary planes to/from rank-1 and
+ * rank+1 with ncclSend/ncclRecv on a comm stream, overlapped with the interior planes. */
+int rtm_get_unique_id(unsigned char id[128]);
+rtm_ctx* rtm_create_dist(int nx, int ny, int nz_global, float dx, float dt,
+                         const float coeffs[6], int rank, int world, const unsigned char id[128],
+                         int device);
+
+/* Host-only plan helpers (no GPU needed; shared by the library and the CPU tests).
+ * rtm_slab_range: rank's owned global planes [*z0, *z0 + *nzl); balanced split
+ *   z0 = rank*nz/world (floor).  RTM_EINVAL if world < 1, rank out of range, or a slab
+ *   would have fewer than 10 planes when world > 1.
+ * rtm_halo_plan: element offsets, within a slab buffer of nx*ny*(nzl+10) floats, of
+ *   [0] send_lo  (owned planes 0..4   -> rank-1),  [1] recv_lo (halo planes -5..-1),
+ *   [2] send_hi  (owned planes nzl-5.. -> rank+1), [3] recv_hi (halo planes nzl..nzl+4);
+ *   *count = 5*nx*ny elements per message; an offset is -1 when that neighbour is absent. */
+int rtm_slab_range(int nz_global, int world, int rank, int* z0, int* nzl);
+int rtm_halo_plan(int nx, int ny, int nzl, int rank, int world, long long offsets[4],
+                  long long* count);
+
+/* Stability bound nu_crit = 2/sqrt(3*S_max), S_max = max_theta -(c0 + 2 sum c_m cos m theta)
+ * (host-only; < 0 on invalid coefficients). */
+double rtm_nu_crit(const float coeffs[6]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RTM_H_ */

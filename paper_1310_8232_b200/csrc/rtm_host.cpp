@@ -1,0 +1,996 @@
+// =====================================================================================
+// Host side of the C ABI (include/rtm.h): validation, CFL check, device buffers, streams,
+// CUDA graphs, source tables, z-slab decomposition with in-process peer copies or NCCL
+// send/recv halo exchange.  All arithmetic of the step runs in
+// the kernels of rtm_kernels.cu; nothing here computes field values.
+// =====================================================================================
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "rtm_internal.h"
+
+using namespace rtm;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                         \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return fail(RTM_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                             \
+    } while (0)
+
+#define NK(call)                                                                              \
+    do {                                                                                      \
+        ncclResult_t r_ = (call);                                                             \
+        if (r_ != ncclSuccess)                                                                \
+            return fail(RTM_ENCCL, "%s failed: %s (%s:%d)", #call, ncclGetErrorString(r_), \
+                        __FILE__, __LINE__);                                                  \
+    } while (0)
+
+#define RET(call)             \
+    do {                      \
+        int rc_ = (call);     \
+        if (rc_ != RTM_OK) return rc_; \
+    } while (0)
+
+struct DeviceGuard {  // restore the caller's current device
+    int saved = -1;
+    DeviceGuard() { cudaGetDevice(&saved); }
+    ~DeviceGuard() {
+        if (saved >= 0) cudaSetDevice(saved);
+    }
+};
+
+struct HostSource {
+    int x, y, z;  // global
+    std::vector<float> samples;
+};
+
+constexpr int GRAPH_PAIRS = 8;  // a captured graph advances 2*GRAPH_PAIRS steps
+
+struct Slab {
+    int dev = 0;
+    int z0 = 0, nzl = 0;
+    bool lo_nb = false, hi_nb = false;
+    float* buf[2] = {nullptr, nullptr};  // nzl+10 planes each
+    float* C = nullptr;                  // nzl planes
+    int* d_step = nullptr;               // [2]
+    unsigned int* d_stats = nullptr;     // [2] velocity check
+    float* d_samples = nullptr;
+    std::vector<DevSource> srcs;
+    std::vector<float> h_samples;
+    cudaStream_t s_own = nullptr, s_comm = nullptr, s_user = nullptr;
+    bool has_user = false;
+    cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
+    CUtensorMap tm[2];
+    int tm_variant = -1;
+    cudaGraphExec_t graph = nullptr;
+    cudaGraph_t graph_def = nullptr;
+    int graph_variant = -1;
+    bool graph_valid = false;
+    cudaStream_t stream() const { return has_user ? s_user : s_own; }
+};
+
+}  // namespace
+
+struct rtm_ctx {
+    int mode = 0;  // 0 single, 1 multi (in-process slabs), 2 dist (NCCL)
+    int nx = 0, ny = 0, nz = 0;  // nz = global planes
+    float dx = 0, dt = 0;
+    float coeffs[6] = {};
+    double nu_crit = 0;
+    std::vector<Slab> slabs;
+    int rank = 0, world = 1;
+    ncclComm_t comm = nullptr;
+    long long step = 0;
+    bool vel_set = false;
+    int tile = -1;
+    int zchunk = 0;  // 0 = auto
+    std::vector<HostSource> sources;
+    bool profiling = false;
+    std::vector<cudaEvent_t> prof_ev;
+    long long prof_launches = 0;        // event pairs recorded in the current rtm_step
+    long long prof_total_launches = 0;  // since rtm_set_profiling / last rtm_kernel_stats
+    double prof_ms = 0;
+    long long launches = 0;
+    float last_ms = 0;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    int num_sms = 148;
+};
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+bool finite_coeffs(const float c[6]) {
+    for (int k = 0; k < 6; ++k)
+        if (!std::isfinite(c[k])) return false;
+    return true;
+}
+
+// S_max = max_theta -(c0 + 2 sum_m c_m cos m theta), sampled on [0, pi] and refined.
+double smax_of(const float c[6]) {
+    auto S = [&](double th) {
+        double s = c[0];
+        for (int m = 1; m <= 5; ++m) s += 2.0 * c[m] * std::cos(m * th);
+        return -s;
+    };
+    const int N = 8192;
+    double best = -1e300, bt = 0;
+    for (int i = 0; i <= N; ++i) {
+        const double th = M_PI * i / N;
+        const double v = S(th);
+        if (v > best) best = v, bt = th;
+    }
+    double lo = std::max(0.0, bt - M_PI / N), hi = std::min(M_PI, bt + M_PI / N);
+    for (int it = 0; it < 100; ++it) {  // golden-section refinement
+        const double a = lo + (hi - lo) * 0.381966, b = lo + (hi - lo) * 0.618034;
+        if (S(a) < S(b)) lo = a; else hi = b;
+    }
+    return std::max(best, S(0.5 * (lo + hi)));
+}
+
+int validate_grid(int nx, int ny, int nz, float dx, float dt, const float* coeffs) {
+    if (nx < 1 || ny < 1 || nz < 1)
+        return fail(RTM_EINVAL, "grid extents must be >= 1 (nx=%d ny=%d nz=%d)", nx, ny, nz);
+    if ((long long)nx * ny > (1LL << 31))
+        return fail(RTM_EINVAL, "nx*ny=%lld exceeds 2^31", (long long)nx * ny);
+    if (!(std::isfinite(dx) && dx > 0)) return fail(RTM_EINVAL, "dx must be finite and > 0");
+    if (!(std::isfinite(dt) && dt > 0)) return fail(RTM_EINVAL, "dt must be finite and > 0");
+    if (!coeffs) return fail(RTM_EINVAL, "coeffs is NULL");
+    if (!finite_coeffs(coeffs)) return fail(RTM_EINVAL, "coeffs must be finite");
+    if (!(smax_of(coeffs) > 0))
+        return fail(RTM_EINVAL, "coeffs do not define a negative-definite 2nd difference (S_max <= 0)");
+    return RTM_OK;
+}
+
+int alloc_slab(rtm_ctx* c, Slab& s) {
+    CK(cudaSetDevice(s.dev));
+    const size_t plane = (size_t)c->nx * c->ny;
+    const size_t nbuf = plane * (s.nzl + 10);
+    for (int b = 0; b < 2; ++b) {
+        if (cudaMalloc(&s.buf[b], nbuf * sizeof(float)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(RTM_ENOMEM, "cudaMalloc of %zu bytes (field %d) failed", nbuf * 4, b);
+        }
+    }
+    if (cudaMalloc(&s.C, plane * s.nzl * sizeof(float)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(RTM_ENOMEM, "cudaMalloc of %zu bytes (C) failed", plane * s.nzl * 4);
+    }
+    CK(cudaMalloc(&s.d_step, 2 * sizeof(int)));
+    CK(cudaMalloc(&s.d_stats, 2 * sizeof(unsigned int)));
+    CK(cudaStreamCreateWithFlags(&s.s_own, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s.s_comm, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&s.ev_bnd, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&s.ev_comm, cudaEventDisableTiming));
+    for (int b = 0; b < 2; ++b) CK(cudaMemsetAsync(s.buf[b], 0, nbuf * sizeof(float), s.s_own));
+    CK(cudaMemsetAsync(s.C, 0, plane * s.nzl * sizeof(float), s.s_own));
+    CK(cudaMemsetAsync(s.d_step, 0, 2 * sizeof(int), s.s_own));
+    CK(cudaStreamSynchronize(s.s_own));
+    return RTM_OK;
+}
+
+void free_slab(Slab& s) {
+    cudaSetDevice(s.dev);
+    if (s.graph) cudaGraphExecDestroy(s.graph);
+    if (s.graph_def) cudaGraphDestroy(s.graph_def);
+    for (int b = 0; b < 2; ++b)
+        if (s.buf[b]) cudaFree(s.buf[b]);
+    if (s.C) cudaFree(s.C);
+    if (s.d_step) cudaFree(s.d_step);
+    if (s.d_stats) cudaFree(s.d_stats);
+    if (s.d_samples) cudaFree(s.d_samples);
+    if (s.ev_bnd) cudaEventDestroy(s.ev_bnd);
+    if (s.ev_comm) cudaEventDestroy(s.ev_comm);
+    if (s.s_own) cudaStreamDestroy(s.s_own);
+    if (s.s_comm) cudaStreamDestroy(s.s_comm);
+    s = Slab();
+}
+
+void destroy_ctx(rtm_ctx* c) {
+    if (!c) return;
+    DeviceGuard g;
+    for (auto& s : c->slabs) {
+        if (s.s_own) {
+            cudaSetDevice(s.dev);
+            cudaStreamSynchronize(s.s_own);
+            cudaStreamSynchronize(s.s_comm);
+        }
+    }
+    if (c->comm) ncclCommDestroy(c->comm);
+    if (!c->slabs.empty()) cudaSetDevice(c->slabs[0].dev);
+    for (auto e : c->prof_ev) cudaEventDestroy(e);
+    if (c->t0) cudaEventDestroy(c->t0);
+    if (c->t1) cudaEventDestroy(c->t1);
+    for (auto& s : c->slabs) free_slab(s);
+    delete c;
+}
+
+rtm_ctx* new_ctx(int nx, int ny, int nz, float dx, float dt, const float* coeffs) {
+    if (validate_grid(nx, ny, nz, dx, dt, coeffs) != RTM_OK) return nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+        cudaGetLastError();
+        fail(RTM_ECUDA, "no CUDA device available (the library has no CPU fallback)");
+        return nullptr;
+    }
+    rtm_ctx* c = new rtm_ctx();
+    c->nx = nx;
+    c->ny = ny;
+    c->nz = nz;
+    c->dx = dx;
+    c->dt = dt;
+    std::memcpy(c->coeffs, coeffs, sizeof c->coeffs);
+    c->nu_crit = 2.0 / std::sqrt(3.0 * smax_of(coeffs));
+    return c;
+}
+
+int finish_ctx(rtm_ctx* c) {
+    CK(cudaSetDevice(c->slabs[0].dev));
+    CK(cudaEventCreate(&c->t0));
+    CK(cudaEventCreate(&c->t1));
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->slabs[0].dev));
+    for (auto& s : c->slabs) RET(alloc_slab(c, s));
+    return RTM_OK;
+}
+
+int resolve_tile(const rtm_ctx* c) {
+    if (c->nx % 4 != 0) return 0;  // 128-bit rows / TMA strides need nx % 4 == 0
+    if (c->tile >= 0) return c->tile;
+    return 1;  // tma64x16k10 (tile sweep)
+}
+
+int ensure_tmaps(rtm_ctx* c, Slab& s, int var) {
+    if (var == 0 || s.tm_variant == var) return RTM_OK;
+    auto enc = encode_fn();
+    if (!enc) return fail(RTM_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    const TileVariant& tv = variant(var);
+    cuuint64_t dims[3] = {(cuuint64_t)c->nx, (cuuint64_t)c->ny, (cuuint64_t)(s.nzl + 10)};
+    cuuint64_t strides[2] = {(cuuint64_t)c->nx * 4, (cuuint64_t)c->nx * c->ny * 4};
+    cuuint32_t box[3] = {(cuuint32_t)(tv.TX + 16), (cuuint32_t)(tv.TY + 10), 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    for (int b = 0; b < 2; ++b) {
+        CUresult r = enc(&s.tm[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, s.buf[b], dims, strides, box,
+                         es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(RTM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    }
+    s.tm_variant = var;
+    return RTM_OK;
+}
+
+// z-chunks for a range of len planes: minimise (wave quantisation) x (chunk-halo re-read).
+int choose_chunks(const rtm_ctx* c, int var, int ntiles, int len) {
+    if (c->zchunk > 0) return std::max(1, (len + c->zchunk - 1) / c->zchunk);
+    int tpb = 0;
+    int occ = tiled_occupancy(var, &tpb);
+    if (occ < 1) occ = 1;
+    const double S = (double)c->num_sms * occ;
+    int best = 1;
+    double bestc = 1e300;
+    const int maxc = std::max(1, len / 8);
+    for (int nc = 1; nc <= maxc; ++nc) {
+        const double units = (double)ntiles * nc;
+        const double waves = units / S;
+        const double eff = std::ceil(waves - 1e-9) / waves;
+        const double zc = (double)len / nc;
+        const double cost = eff * (1.0 + 2.5 / zc);
+        if (cost < bestc - 1e-12) bestc = cost, best = nc;
+    }
+    return best;
+}
+
+void fill_params(const rtm_ctx* c, const Slab& s, int parity, StencilParams& p) {
+    std::memset(&p, 0, sizeof p);
+    p.nx = c->nx;
+    p.ny = c->ny;
+    p.nzl = s.nzl;
+    p.plane = (long long)c->nx * c->ny;
+    p.coef[0] = 3.0f * c->coeffs[0];
+    for (int k = 1; k < 6; ++k) p.coef[k] = c->coeffs[k];
+    p.u = s.buf[parity];
+    p.next = s.buf[parity ^ 1];
+    p.C = s.C;
+    p.d_step = s.d_step;
+    p.parity = parity;
+    p.nsrc = (int)s.srcs.size();
+    for (int k = 0; k < p.nsrc; ++k) p.src[k] = s.srcs[k];
+    p.samples = s.d_samples;
+}
+
+// Launch the stencil on planes [b0,b0+l0) (+ [b1,b1+l1) if l1 > 0) of slab s.
+int launch_stencil(rtm_ctx* c, Slab& s, int parity, int b0, int l0, int b1, int l1,
+                   int write_next, cudaStream_t st) {
+    const int var = resolve_tile(c);
+    StencilParams p;
+    fill_params(c, s, parity, p);
+    p.write_next = write_next;
+    p.nranges = l1 > 0 ? 2 : 1;
+    p.r_begin[0] = b0;
+    p.r_len[0] = l0;
+    p.r_begin[1] = b1;
+    p.r_len[1] = l1 > 0 ? l1 : 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->profiling) {
+        const size_t k = 2 * (size_t)c->prof_launches;
+        while (c->prof_ev.size() < k + 2) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            c->prof_ev.push_back(e);
+        }
+        e0 = c->prof_ev[k];
+        e1 = c->prof_ev[k + 1];
+        CK(cudaEventRecord(e0, st));
+    }
+    if (var == 0) {
+        CK(launch_naive(p, st));
+    } else {
+        RET(ensure_tmaps(c, s, var));
+        const TileVariant& tv = variant(var);
+        p.tiles_x = (c->nx + tv.TX - 1) / tv.TX;
+        p.tiles_y = (c->ny + tv.TY - 1) / tv.TY;
+        const int nt = p.tiles_x * p.tiles_y;
+        p.r_chunks[0] = choose_chunks(c, var, nt, l0);
+        p.r_chunks[1] = l1 > 0 ? choose_chunks(c, var, nt, l1) : 0;
+        CK(launch_tiled(var, s.tm[parity], p, st));
+    }
+    if (c->profiling) {
+        CK(cudaEventRecord(e1, st));
+        ++c->prof_launches;
+    }
+    ++c->launches;
+    return RTM_OK;
+}
+
+int collect_profile(rtm_ctx* c) {
+    if (!c->profiling) return RTM_OK;
+    for (long long k = 0; k < c->prof_launches; ++k) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, c->prof_ev[2 * k], c->prof_ev[2 * k + 1]));
+        c->prof_ms += ms;
+    }
+    c->prof_total_launches += c->prof_launches;
+    return RTM_OK;
+}
+
+int build_graph(rtm_ctx* c, Slab& s) {
+    const int var = resolve_tile(c);
+    if (s.graph_valid && s.graph_variant == var) return RTM_OK;
+    if (s.graph) cudaGraphExecDestroy(s.graph), s.graph = nullptr;
+    if (s.graph_def) cudaGraphDestroy(s.graph_def), s.graph_def = nullptr;
+    RET(ensure_tmaps(c, s, var));
+    CK(cudaStreamBeginCapture(s.s_own, cudaStreamCaptureModeThreadLocal));
+    const long long saved = c->launches;
+    int rc = RTM_OK;
+    for (int k = 0; k < 2 * GRAPH_PAIRS && rc == RTM_OK; ++k)
+        rc = launch_stencil(c, s, k & 1, 0, s.nzl, 0, 0, 1, s.s_own);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(s.s_own, &g);
+    c->launches = saved;
+    if (rc != RTM_OK) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    if (e != cudaSuccess) return fail(RTM_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
+    s.graph_def = g;
+    CK(cudaGraphInstantiate(&s.graph, g, 0));
+    s.graph_valid = true;
+    s.graph_variant = var;
+    return RTM_OK;
+}
+
+void invalidate_graphs(rtm_ctx* c) {
+    for (auto& s : c->slabs) s.graph_valid = false;
+}
+
+int upload_sources(rtm_ctx* c, Slab& s) {
+    CK(cudaSetDevice(s.dev));
+    if (s.d_samples) {
+        CK(cudaStreamSynchronize(s.stream()));
+        CK(cudaFree(s.d_samples));
+        s.d_samples = nullptr;
+    }
+    if (!s.h_samples.empty()) {
+        CK(cudaMalloc(&s.d_samples, s.h_samples.size() * sizeof(float)));
+        CK(cudaMemcpy(s.d_samples, s.h_samples.data(), s.h_samples.size() * sizeof(float),
+                      cudaMemcpyHostToDevice));
+    }
+    invalidate_graphs(c);
+    return RTM_OK;
+}
+
+int step_single(rtm_ctx* c, int nsteps) {
+    Slab& s = c->slabs[0];
+    cudaStream_t st = s.stream();
+    int k = 0;
+    while (k < nsteps) {
+        const int parity = (int)(c->step & 1);
+        if (!c->profiling && parity == 0 && nsteps - k >= 2 * GRAPH_PAIRS) {
+            RET(build_graph(c, s));
+            CK(cudaGraphLaunch(s.graph, st));
+            c->step += 2 * GRAPH_PAIRS;
+            c->launches += 2 * GRAPH_PAIRS;
+            k += 2 * GRAPH_PAIRS;
+            continue;
+        }
+        RET(launch_stencil(c, s, parity, 0, s.nzl, 0, 0, 1, st));
+        ++c->step;
+        ++k;
+    }
+    return RTM_OK;
+}
+
+int exchange_local(rtm_ctx* c, int parity_next) {
+    const int G = (int)c->slabs.size();
+    const size_t plane = (size_t)c->nx * c->ny;
+    const size_t bytes = 5 * plane * sizeof(float);
+    for (int r = 0; r < G; ++r) {
+        Slab& s = c->slabs[r];
+        CK(cudaSetDevice(s.dev));
+        for (int d = -1; d <= 1; ++d)
+            if (r + d >= 0 && r + d < G) CK(cudaStreamWaitEvent(s.s_comm, c->slabs[r + d].ev_bnd, 0));
+        float* dst = s.buf[parity_next];
+        if (s.lo_nb) {
+            const Slab& n = c->slabs[r - 1];
+            CK(cudaMemcpyPeerAsync(dst, s.dev, n.buf[parity_next] + (size_t)n.nzl * plane, n.dev,
+                                   bytes, s.s_comm));
+        }
+        if (s.hi_nb) {
+            const Slab& n = c->slabs[r + 1];
+            CK(cudaMemcpyPeerAsync(dst + (size_t)(s.nzl + 5) * plane, s.dev,
+                                   n.buf[parity_next] + 5 * plane, n.dev, bytes, s.s_comm));
+        }
+        CK(cudaEventRecord(s.ev_comm, s.s_comm));
+    }
+    return RTM_OK;
+}
+
+int exchange_nccl(rtm_ctx* c, int parity_next) {
+    Slab& s = c->slabs[0];
+    const size_t plane = (size_t)c->nx * c->ny;
+    const size_t cnt = 5 * plane;
+    CK(cudaStreamWaitEvent(s.s_comm, s.ev_bnd, 0));
+    float* b = s.buf[parity_next];
+    NK(ncclGroupStart());
+    if (s.lo_nb) {
+        NK(ncclSend(b + 5 * plane, cnt, ncclFloat32, c->rank - 1, c->comm, s.s_comm));
+        NK(ncclRecv(b, cnt, ncclFloat32, c->rank - 1, c->comm, s.s_comm));
+    }
+    if (s.hi_nb) {
+        NK(ncclSend(b + (size_t)s.nzl * plane, cnt, ncclFloat32, c->rank + 1, c->comm, s.s_comm));
+        NK(ncclRecv(b + (size_t)(s.nzl + 5) * plane, cnt, ncclFloat32, c->rank + 1, c->comm,
+                    s.s_comm));
+    }
+    NK(ncclGroupEnd());
+    CK(cudaEventRecord(s.ev_comm, s.s_comm));
+    return RTM_OK;
+}
+
+// G > 1 step: boundary planes first, exchange on the comm stream, interior concurrently.
+int step_slabs(rtm_ctx* c, int nsteps) {
+    const int G = (int)c->slabs.size();
+    for (int k = 0; k < nsteps; ++k) {
+        const int parity = (int)(c->step & 1);
+        for (int r = 0; r < G; ++r) {
+            Slab& s = c->slabs[r];
+            CK(cudaSetDevice(s.dev));
+            for (int d = -1; d <= 1; ++d)  // previous exchange done (reads and writes)
+                if (r + d >= 0 && r + d < G) CK(cudaStreamWaitEvent(s.stream(), c->slabs[r + d].ev_comm, 0));
+            if (s.lo_nb || s.hi_nb) {
+                const int b0 = s.lo_nb ? 0 : s.nzl - 5;
+                const int l0 = 5;
+                const int b1 = s.nzl - 5, l1 = (s.lo_nb && s.hi_nb) ? 5 : 0;
+                RET(launch_stencil(c, s, parity, b0, l0, b1, l1, 0, s.stream()));
+            }
+            CK(cudaEventRecord(s.ev_bnd, s.stream()));
+        }
+        if (c->mode == 2) RET(exchange_nccl(c, parity ^ 1));
+        else RET(exchange_local(c, parity ^ 1));
+        for (int r = 0; r < G; ++r) {
+            Slab& s = c->slabs[r];
+            CK(cudaSetDevice(s.dev));
+            const int ib = s.lo_nb ? 5 : 0;
+            const int ie = s.hi_nb ? s.nzl - 5 : s.nzl;
+            RET(launch_stencil(c, s, parity, ib, ie - ib, 0, 0, 1, s.stream()));
+        }
+        ++c->step;
+    }
+    for (int r = 0; r < G; ++r) {  // join: the field is complete when the step returns
+        Slab& s = c->slabs[r];
+        CK(cudaSetDevice(s.dev));
+        for (int d = -1; d <= 1; ++d)
+            if (r + d >= 0 && r + d < G) CK(cudaStreamWaitEvent(s.stream(), c->slabs[r + d].ev_comm, 0));
+    }
+    return RTM_OK;
+}
+
+int sync_all(rtm_ctx* c) {
+    for (auto& s : c->slabs) {
+        CK(cudaSetDevice(s.dev));
+        CK(cudaStreamSynchronize(s.stream()));
+        CK(cudaStreamSynchronize(s.s_comm));
+    }
+    if (c->comm) {
+        ncclResult_t ar;
+        NK(ncclCommGetAsyncError(c->comm, &ar));
+        if (ar != ncclSuccess) return fail(RTM_ENCCL, "NCCL async error: %s", ncclGetErrorString(ar));
+    }
+    return RTM_OK;
+}
+
+// Copy host slab arrays (x fastest) into/out of the interior planes of a device buffer.
+int h2d_planes(rtm_ctx* c, Slab& s, float* dst_base, const float* host, cudaStream_t st) {
+    const size_t plane = (size_t)c->nx * c->ny;
+    CK(cudaMemcpyAsync(dst_base, host, plane * s.nzl * sizeof(float), cudaMemcpyHostToDevice, st));
+    return RTM_OK;
+}
+
+int set_velocity_impl(rtm_ctx* c, const float* v, bool device_ptr) {
+    c->vel_set = false;
+    const size_t plane = (size_t)c->nx * c->ny;
+    for (auto& s : c->slabs) {
+        CK(cudaSetDevice(s.dev));
+        cudaStream_t st = s.stream();
+        const float* src;
+        if (device_ptr) {
+            src = v + (size_t)(s.z0 - c->slabs[0].z0) * plane;
+        } else {
+            // stage v in C and convert in place
+            const float* h = v + (c->mode == 1 ? (size_t)s.z0 * plane : 0);
+            RET(h2d_planes(c, s, s.C, h, st));
+            src = s.C;
+        }
+        CK(cudaMemsetAsync(s.d_stats, 0, 2 * sizeof(unsigned int), st));
+        CK(launch_velocity(src, s.C, (long long)plane * s.nzl, (double)c->dt, (double)c->dx,
+                           s.d_stats, st));
+    }
+    float vmax = 0.0f;
+    unsigned long long bad = 0;
+    for (auto& s : c->slabs) {
+        CK(cudaSetDevice(s.dev));
+        unsigned int h[2];
+        CK(cudaMemcpyAsync(h, s.d_stats, sizeof h, cudaMemcpyDeviceToHost, s.stream()));
+        CK(cudaStreamSynchronize(s.stream()));
+        float m;
+        std::memcpy(&m, &h[0], 4);
+        vmax = std::max(vmax, m);
+        bad += h[1];
+    }
+    if (bad) return fail(RTM_EINVAL, "velocity has %llu non-finite or non-positive values", bad);
+    const double nu = (double)vmax * (double)c->dt / (double)c->dx;
+    if (nu > c->nu_crit)
+        return fail(RTM_ECFL, "CFL violated: max(v)*dt/dx = %.6f > nu_crit = %.6f (max v = %g m/s)",
+                    nu, c->nu_crit, (double)vmax);
+    c->vel_set = true;
+    return RTM_OK;
+}
+
+int reset_impl(rtm_ctx* c, const float* u, const float* up) {
+    const size_t plane = (size_t)c->nx * c->ny;
+    for (auto& s : c->slabs) {
+        CK(cudaSetDevice(s.dev));
+        cudaStream_t st = s.stream();
+        CK(cudaStreamSynchronize(s.s_comm));
+        const size_t nbuf = plane * (s.nzl + 10);
+        for (int b = 0; b < 2; ++b) CK(cudaMemsetAsync(s.buf[b], 0, nbuf * sizeof(float), st));
+        const size_t off = c->mode == 1 ? (size_t)s.z0 * plane : 0;
+        if (u) RET(h2d_planes(c, s, s.buf[0] + 5 * plane, u + off, st));
+        if (up) RET(h2d_planes(c, s, s.buf[1] + 5 * plane, up + off, st));
+        CK(cudaMemsetAsync(s.d_step, 0, 2 * sizeof(int), st));
+    }
+    c->step = 0;
+    // G > 1: fill the halo planes of u^0 and u^{-1} from the neighbours' initial data
+    if (c->slabs.size() > 1 || c->mode == 2) {
+        for (int par = 0; par < 2; ++par) {
+            for (auto& s : c->slabs) {
+                CK(cudaSetDevice(s.dev));
+                CK(cudaEventRecord(s.ev_bnd, s.stream()));
+            }
+            if (c->mode == 2) RET(exchange_nccl(c, par));
+            else RET(exchange_local(c, par));
+        }
+    }
+    return sync_all(c);
+}
+
+int read_impl(rtm_ctx* c, float* out, int which /*0 = u^n, 1 = u^{n-1}*/) {
+    const size_t plane = (size_t)c->nx * c->ny;
+    const int par = (int)((c->step + which) & 1);
+    for (auto& s : c->slabs) {
+        CK(cudaSetDevice(s.dev));
+        const size_t off = c->mode == 1 ? (size_t)s.z0 * plane : 0;
+        CK(cudaMemcpyAsync(out + off, s.buf[par] + 5 * plane, plane * s.nzl * sizeof(float),
+                           cudaMemcpyDeviceToHost, s.stream()));
+    }
+    return sync_all(c);
+}
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+const char* rtm_last_error(void) { return g_err.c_str(); }
+
+double rtm_nu_crit(const float coeffs[6]) {
+    if (!coeffs || !finite_coeffs(coeffs)) return -1.0;
+    const double s = smax_of(coeffs);
+    return s > 0 ? 2.0 / std::sqrt(3.0 * s) : -1.0;
+}
+
+int rtm_slab_range(int nz_global, int world, int rank, int* z0, int* nzl) {
+    if (world < 1 || rank < 0 || rank >= world || nz_global < 1 || !z0 || !nzl)
+        return fail(RTM_EINVAL, "invalid slab request (nz=%d world=%d rank=%d)", nz_global, world, rank);
+    const long long a = (long long)rank * nz_global / world;
+    const long long b = (long long)(rank + 1) * nz_global / world;
+    if (world > 1 && (long long)nz_global / world < 10)
+        return fail(RTM_EINVAL, "nz/world = %d/%d < 10 planes per slab", nz_global, world);
+    *z0 = (int)a;
+    *nzl = (int)(b - a);
+    return RTM_OK;
+}
+
+int rtm_halo_plan(int nx, int ny, int nzl, int rank, int world, long long offsets[4],
+                  long long* count) {
+    if (nx < 1 || ny < 1 || nzl < 1 || world < 1 || rank < 0 || rank >= world || !offsets || !count)
+        return fail(RTM_EINVAL, "invalid halo plan request");
+    if (world > 1 && nzl < 10) return fail(RTM_EINVAL, "nzl=%d < 10", nzl);
+    const long long plane = (long long)nx * ny;
+    const bool lo = rank > 0, hi = rank < world - 1;
+    offsets[0] = lo ? 5 * plane : -1;
+    offsets[1] = lo ? 0 : -1;
+    offsets[2] = hi ? (long long)nzl * plane : -1;
+    offsets[3] = hi ? (long long)(nzl + 5) * plane : -1;
+    *count = 5 * plane;
+    return RTM_OK;
+}
+
+int rtm_num_tiles(void) { return num_variants(); }
+const char* rtm_tile_name(int id) {
+    if (id < 0 || id >= num_variants()) return nullptr;
+    return variant(id).name;
+}
+
+rtm_ctx* rtm_create(int nx, int ny, int nz, float dx, float dt, const float coeffs[6]) {
+    DeviceGuard g;
+    rtm_ctx* c = new_ctx(nx, ny, nz, dx, dt, coeffs);
+    if (!c) return nullptr;
+    c->mode = 0;
+    Slab s;
+    cudaGetDevice(&s.dev);
+    s.z0 = 0;
+    s.nzl = nz;
+    c->slabs.push_back(s);
+    if (finish_ctx(c) != RTM_OK) {
+        std::string e = g_err;
+        destroy_ctx(c);
+        g_err = e;
+        return nullptr;
+    }
+    return c;
+}
+
+rtm_ctx* rtm_create_multi(int nx, int ny, int nz, float dx, float dt, const float coeffs[6],
+                          int nslabs, const int* devices) {
+    DeviceGuard g;
+    if (nslabs < 1 || !devices) {
+        fail(RTM_EINVAL, "nslabs must be >= 1 and devices non-NULL");
+        return nullptr;
+    }
+    int z0, nzl;
+    for (int r = 0; r < nslabs; ++r)
+        if (rtm_slab_range(nz, nslabs, r, &z0, &nzl) != RTM_OK) return nullptr;
+    int ndev = 0;
+    cudaGetDeviceCount(&ndev);
+    for (int r = 0; r < nslabs; ++r)
+        if (devices[r] < 0 || devices[r] >= ndev) {
+            fail(RTM_EINVAL, "devices[%d] = %d is not a CUDA device (count %d)", r, devices[r], ndev);
+            return nullptr;
+        }
+    rtm_ctx* c = new_ctx(nx, ny, nz, dx, dt, coeffs);
+    if (!c) return nullptr;
+    c->mode = 1;
+    for (int r = 0; r < nslabs; ++r) {
+        Slab s;
+        s.dev = devices[r];
+        rtm_slab_range(nz, nslabs, r, &s.z0, &s.nzl);
+        s.lo_nb = r > 0;
+        s.hi_nb = r < nslabs - 1;
+        c->slabs.push_back(s);
+    }
+    for (int r = 0; r < nslabs; ++r)  // best effort peer access (copies work either way)
+        for (int q = 0; q < nslabs; ++q)
+            if (devices[r] != devices[q]) {
+                int can = 0;
+                cudaDeviceCanAccessPeer(&can, devices[r], devices[q]);
+                if (can) {
+                    cudaSetDevice(devices[r]);
+                    cudaDeviceEnablePeerAccess(devices[q], 0);
+                    cudaGetLastError();
+                }
+            }
+    if (finish_ctx(c) != RTM_OK) {
+        std::string e = g_err;
+        destroy_ctx(c);
+        g_err = e;
+        return nullptr;
+    }
+    return c;
+}
+
+int rtm_get_unique_id(unsigned char id[128]) {
+    if (!id) return fail(RTM_EINVAL, "id is NULL");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId u;
+    NK(ncclGetUniqueId(&u));
+    std::memcpy(id, &u, 128);
+    return RTM_OK;
+}
+
+rtm_ctx* rtm_create_dist(int nx, int ny, int nz_global, float dx, float dt,
+                         const float coeffs[6], int rank, int world, const unsigned char id[128],
+                         int device) {
+    DeviceGuard g;
+    int z0, nzl;
+    if (rtm_slab_range(nz_global, world, rank, &z0, &nzl) != RTM_OK) return nullptr;
+    if (!id) {
+        fail(RTM_EINVAL, "id is NULL");
+        return nullptr;
+    }
+    int ndev = 0;
+    cudaGetDeviceCount(&ndev);
+    if (device < 0 || device >= ndev) {
+        fail(RTM_EINVAL, "device %d is not a CUDA device (count %d)", device, ndev);
+        return nullptr;
+    }
+    rtm_ctx* c = new_ctx(nx, ny, nz_global, dx, dt, coeffs);
+    if (!c) return nullptr;
+    c->mode = 2;
+    c->rank = rank;
+    c->world = world;
+    Slab s;
+    s.dev = device;
+    s.z0 = z0;
+    s.nzl = nzl;
+    s.lo_nb = rank > 0;
+    s.hi_nb = rank < world - 1;
+    c->slabs.push_back(s);
+    if (finish_ctx(c) != RTM_OK) {
+        std::string e = g_err;
+        destroy_ctx(c);
+        g_err = e;
+        return nullptr;
+    }
+    cudaSetDevice(device);
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    ncclResult_t r = ncclCommInitRank(&c->comm, world, u, rank);
+    if (r != ncclSuccess) {
+        c->comm = nullptr;
+        destroy_ctx(c);
+        fail(RTM_ENCCL, "ncclCommInitRank failed: %s", ncclGetErrorString(r));
+        return nullptr;
+    }
+    return c;
+}
+
+void rtm_destroy(rtm_ctx* ctx) { destroy_ctx(ctx); }
+
+int rtm_set_velocity(rtm_ctx* c, const float* v) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    if (!v) return fail(RTM_EINVAL, "v is NULL");
+    DeviceGuard g;
+    return set_velocity_impl(c, v, false);
+}
+
+int rtm_set_velocity_device(rtm_ctx* c, const float* d_v) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    if (!d_v) return fail(RTM_EINVAL, "d_v is NULL");
+    if (c->slabs.size() != 1) return fail(RTM_EINVAL, "device velocity needs a single-slab context");
+    DeviceGuard g;
+    return set_velocity_impl(c, d_v, true);
+}
+
+int rtm_inject_source(rtm_ctx* c, int ix, int iy, int iz, const float* samples, int nsamples) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    if (ix < 0 || ix >= c->nx || iy < 0 || iy >= c->ny || iz < 0 || iz >= c->nz)
+        return fail(RTM_EINVAL, "source (%d,%d,%d) outside the %dx%dx%d interior", ix, iy, iz,
+                    c->nx, c->ny, c->nz);
+    if (nsamples < 0 || (nsamples > 0 && !samples))
+        return fail(RTM_EINVAL, "nsamples must be >= 0 with non-NULL samples");
+    for (int n = 0; n < nsamples; ++n)
+        if (!std::isfinite(samples[n])) return fail(RTM_EINVAL, "samples[%d] is not finite", n);
+    if ((int)c->sources.size() >= RTM_MAX_SOURCES)
+        return fail(RTM_EINVAL, "at most %d sources", RTM_MAX_SOURCES);
+    DeviceGuard g;
+    HostSource hs{ix, iy, iz, std::vector<float>(samples, samples + nsamples)};
+    c->sources.push_back(hs);
+    for (auto& s : c->slabs) {
+        if (iz < s.z0 || iz >= s.z0 + s.nzl) continue;  // owned by another slab / rank
+        DevSource d;
+        d.x = ix;
+        d.y = iy;
+        d.z = iz - s.z0;
+        d.nsamples = nsamples;
+        d.offset = (long long)s.h_samples.size();
+        s.h_samples.insert(s.h_samples.end(), samples, samples + nsamples);
+        s.srcs.push_back(d);
+        RET(upload_sources(c, s));
+    }
+    return RTM_OK;
+}
+
+int rtm_step(rtm_ctx* c, int nsteps) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    if (nsteps < 0) return fail(RTM_EINVAL, "nsteps must be >= 0");
+    if (!c->vel_set) return fail(RTM_ESTATE, "rtm_step before a successful rtm_set_velocity");
+    DeviceGuard g;
+    Slab& s0 = c->slabs[0];
+    CK(cudaSetDevice(s0.dev));
+    c->prof_launches = 0;
+    CK(cudaEventRecord(c->t0, s0.stream()));
+    if (c->mode == 0) {
+        RET(step_single(c, nsteps));
+    } else {
+        for (size_t r = 1; r < c->slabs.size(); ++r) {  // start together
+            CK(cudaSetDevice(c->slabs[r].dev));
+            CK(cudaStreamWaitEvent(c->slabs[r].stream(), c->t0, 0));
+        }
+        RET(step_slabs(c, nsteps));
+        CK(cudaSetDevice(s0.dev));
+        for (size_t r = 1; r < c->slabs.size(); ++r) {
+            CK(cudaEventRecord(c->slabs[r].ev_bnd, c->slabs[r].stream()));
+            CK(cudaStreamWaitEvent(s0.stream(), c->slabs[r].ev_bnd, 0));
+        }
+    }
+    CK(cudaSetDevice(s0.dev));
+    CK(cudaEventRecord(c->t1, s0.stream()));
+    RET(sync_all(c));
+    CK(cudaEventElapsedTime(&c->last_ms, c->t0, c->t1));
+    RET(collect_profile(c));
+    c->prof_launches = 0;
+    return RTM_OK;
+}
+
+int rtm_read_field(rtm_ctx* c, float* out) {
+    if (!c || !out) return fail(RTM_EINVAL, "NULL argument");
+    DeviceGuard g;
+    return read_impl(c, out, 0);
+}
+
+int rtm_read_fields(rtm_ctx* c, float* u, float* up) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    DeviceGuard g;
+    if (u) RET(read_impl(c, u, 0));
+    if (up) RET(read_impl(c, up, 1));
+    return RTM_OK;
+}
+
+int rtm_read_field_device(rtm_ctx* c, float* d_out) {
+    if (!c || !d_out) return fail(RTM_EINVAL, "NULL argument");
+    if (c->slabs.size() != 1) return fail(RTM_EINVAL, "device readback needs a single-slab context");
+    DeviceGuard g;
+    Slab& s = c->slabs[0];
+    CK(cudaSetDevice(s.dev));
+    const size_t plane = (size_t)c->nx * c->ny;
+    CK(cudaMemcpyAsync(d_out, s.buf[c->step & 1] + 5 * plane, plane * s.nzl * sizeof(float),
+                       cudaMemcpyDeviceToDevice, s.stream()));
+    return RTM_OK;
+}
+
+int rtm_set_fields(rtm_ctx* c, const float* u, const float* up) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    DeviceGuard g;
+    return reset_impl(c, u, up);
+}
+
+int rtm_reset(rtm_ctx* c) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    DeviceGuard g;
+    if (c->mode == 0) {  // enqueue only (the bench times reset inside a step)
+        Slab& s = c->slabs[0];
+        CK(cudaSetDevice(s.dev));
+        const size_t nbuf = (size_t)c->nx * c->ny * (s.nzl + 10);
+        for (int b = 0; b < 2; ++b) CK(cudaMemsetAsync(s.buf[b], 0, nbuf * sizeof(float), s.stream()));
+        CK(cudaMemsetAsync(s.d_step, 0, 2 * sizeof(int), s.stream()));
+        c->step = 0;
+        return RTM_OK;
+    }
+    return reset_impl(c, nullptr, nullptr);
+}
+
+long long rtm_step_count(rtm_ctx* c) { return c ? c->step : -1; }
+
+int rtm_set_tile(rtm_ctx* c, int tile_id) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    if (tile_id < -1 || tile_id >= num_variants())
+        return fail(RTM_EINVAL, "unknown tile id %d (valid: -1 .. %d)", tile_id, num_variants() - 1);
+    if (tile_id > 0 && c->nx % 4 != 0)
+        return fail(RTM_EINVAL, "tiled variants need nx %% 4 == 0 (nx=%d)", c->nx);
+    c->tile = tile_id;
+    invalidate_graphs(c);
+    return RTM_OK;
+}
+
+int rtm_get_tile(rtm_ctx* c) { return c ? resolve_tile(c) : -1; }
+
+int rtm_set_zchunk(rtm_ctx* c, int planes) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    if (planes < 0) return fail(RTM_EINVAL, "planes must be >= 0");
+    c->zchunk = planes;
+    invalidate_graphs(c);
+    return RTM_OK;
+}
+
+int rtm_set_stream(rtm_ctx* c, void* stream) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    if (c->slabs.size() != 1)
+        return fail(RTM_EINVAL, "rtm_set_stream needs a single-slab (single-GPU or distributed) context");
+    Slab& s = c->slabs[0];
+    DeviceGuard g;
+    CK(cudaSetDevice(s.dev));
+    CK(cudaStreamSynchronize(s.stream()));
+    s.has_user = stream != nullptr;
+    s.s_user = static_cast<cudaStream_t>(stream);
+    return RTM_OK;
+}
+
+float rtm_last_elapsed_ms(rtm_ctx* c) { return c ? c->last_ms : -1.0f; }
+
+int rtm_set_profiling(rtm_ctx* c, int on) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    c->profiling = on != 0;
+    c->prof_ms = 0;
+    c->prof_launches = 0;
+    c->prof_total_launches = 0;
+    return RTM_OK;
+}
+
+int rtm_kernel_stats(rtm_ctx* c, long long* launches, double* total_ms) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    if (launches) *launches = c->prof_total_launches;
+    if (total_ms) *total_ms = c->prof_ms;
+    c->prof_total_launches = 0;
+    c->prof_ms = 0;
+    return RTM_OK;
+}
+
+long long rtm_launch_count(rtm_ctx* c) { return c ? c->launches : -1; }
+
+}  // extern "C"

@@ -1,0 +1,62 @@
+// Internal interface between the host library (rtm_host.cpp) and the kernels (rtm_kernels.cu).
+// Not installed, not part of the C ABI (include/rtm.h is).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "../../include/rtm.h"
+
+namespace rtm {
+
+constexpr int RADIUS = 5;  // "five points (cells) in each direction"
+
+struct DevSource {       // a source owned by this slab, LOCAL coordinates
+    int x, y, z;         // z = owned plane index (0..nzl-1)
+    int nsamples;
+    long long offset;    // into StencilParams::samples
+};
+
+// Everything a stencil launch needs.  Passed by value (__grid_constant__).
+struct StencilParams {
+    int nx, ny, nzl;           // interior extents of this slab
+    long long plane;           // nx*ny
+    float coef[6];             // coef[0] = 3*c0 (fp32, host-folded), coef[1..5] = c1..c5
+    const float* u;            // u^n buffer base (nzl+10 planes, plane 0 = first halo plane)
+    float* next;               // u^{n-1} buffer base, overwritten in place by u^{n+1}
+    const float* C;            // C(p), nzl planes
+    int* d_step;               // step counter slots [2]; this launch reads d_step[parity]
+    int parity;                // (global step) & 1
+    int write_next;            // 1: block 0 writes d_step[parity^1] = n + 1
+    int nranges;               // 1 or 2 z-ranges of owned planes
+    int r_begin[2], r_len[2];  // ranges [r_begin, r_begin + r_len)
+    int r_chunks[2];           // z-chunks per range (tiled kernel work units)
+    int tiles_x, tiles_y;      // tiled kernel: xy tiles
+    int nsrc;
+    DevSource src[RTM_MAX_SOURCES];
+    const float* samples;
+};
+
+struct TileVariant {
+    const char* name;
+    int TX, TY, K, MINB;       // tile (x, y), TMA ring depth (planes), min blocks per SM
+};
+
+// Variant table: index 0 is the naive kernel, 1.. the TMA-tiled kernels.
+int num_variants();
+const TileVariant& variant(int id);
+
+// Dynamic shared memory of a tiled variant (bytes).
+size_t tiled_smem_bytes(int id);
+// Max resident blocks per SM of a tiled variant (after opting in to its smem), or <0 on error.
+int tiled_occupancy(int id, int* threads_per_block);
+
+cudaError_t launch_tiled(int id, const CUtensorMap& tm, const StencilParams& p, cudaStream_t s);
+cudaError_t launch_naive(const StencilParams& p, cudaStream_t s);
+
+// a1: C = fp32((double(v)*dt/dx)^2), stats[0] = max(v) bits (v > 0), stats[1] = count of
+// invalid (non-finite or <= 0) velocities.  v and C may alias.
+cudaError_t launch_velocity(const float* v, float* C, long long n, double dt, double dx,
+                            unsigned int* stats, cudaStream_t s);
+
+}  // namespace rtm

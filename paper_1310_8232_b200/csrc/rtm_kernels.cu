@@ -1,0 +1,453 @@
+// =====================================================================================
+// sm_100a kernels of the RTM 3D-model step (arxiv 1310.8232, §2
+// Algorithm 1 "calculate 3D model"): radius-5 31-point star, 2nd-order leapfrog, fused
+// point-source injection.
+//
+//   k_tiled  (K1/K2/K3): one CTA per (xy tile, z-chunk) work unit.  The u planes of the
+//            tile plus a 5-cell x/y halo are staged into a K-deep shared-memory ring by TMA
+//            (cp.async.bulk.tensor.3d, OOB zero fill = the x/y Dirichlet halo), completion
+//            tracked by one mbarrier per slot.  Each thread owns 4 consecutive x points
+//            (128-bit accesses) of one row and streams along z with an 11-plane register
+//            queue; y/x neighbours come from the staged plane.  u_prev and C are streamed
+//            with 128-bit loads one plane ahead; u_next is stored in place over u_prev.
+//            Sources registered on the slab are added in the epilogue (fused a3).
+//   k_naive  (K5): one thread per point, global loads; same per-point expression, so its
+//            output is bitwise identical to k_tiled's.
+//   k_velocity (a1): C(p) = fp32((double(v)*dt/dx)^2) + max|v| and validity for the CFL check.
+//
+// The blocked traversal replaces the paper's CPU cache blocking (the
+// (b_i, b_j, b_k) blocksize) by an xy tile streamed along z; see DESIGN.md §Kernels.
+// =====================================================================================
+#include "rtm_internal.h"
+
+#include <cstdio>
+
+namespace rtm {
+
+// ------------------------------------------------------------------------------------
+// The per-point update.  z[k], y[k], x[k] are u at offsets k-5 along each axis (index 5 is
+// the point itself, shared by all three).  ONE expression for every kernel, so all
+// variants are bitwise identical.  Order: centre * 3c0, then z, y, x pairs from the
+// nearest to the farthest offset, then the leapfrog.
+__device__ __forceinline__ float rtm_point(const float (&z)[11], const float (&y)[11],
+                                           const float (&x)[11], float up, float C,
+                                           const float (&c)[6]) {
+    float acc = __fmul_rn(c[0], z[5]);
+#pragma unroll
+    for (int m = 1; m <= 5; ++m) acc = __fmaf_rn(c[m], __fadd_rn(z[5 - m], z[5 + m]), acc);
+#pragma unroll
+    for (int m = 1; m <= 5; ++m) acc = __fmaf_rn(c[m], __fadd_rn(y[5 - m], y[5 + m]), acc);
+#pragma unroll
+    for (int m = 1; m <= 5; ++m) acc = __fmaf_rn(c[m], __fadd_rn(x[5 - m], x[5 + m]), acc);
+    return __fmaf_rn(C, acc, __fmaf_rn(2.0f, z[5], -up));
+}
+
+// ------------------------------------------------------------------------------------
+// PTX helpers: mbarrier + TMA
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int x, int y, int z,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ float4 ld_stream4(const float* p) {  // read-once stream, evict-first
+    return __ldcs(reinterpret_cast<const float4*>(p));
+}
+__device__ __forceinline__ void st_stream4(float* p, float4 v) {
+    __stcs(reinterpret_cast<float4*>(p), v);
+}
+__device__ __forceinline__ float comp(const float4& v, int i) {
+    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+
+// Add the samples of the sources owned by this thread's 4-point column at plane z.
+__device__ __forceinline__ void add_sources(const StencilParams& p, uint64_t mask, int x, int z,
+                                            float (&out)[4]) {
+    while (mask) {
+        const int s = __ffsll(static_cast<long long>(mask)) - 1;
+        mask &= mask - 1;
+        const DevSource& src = p.src[s];
+        if (src.z == z) {
+            const int n = *reinterpret_cast<volatile const int*>(&p.d_step[p.parity]);
+            if (n < src.nsamples) {
+                const float w = p.samples[src.offset + n];
+                const int i = src.x - x;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (k == i) out[k] = __fadd_rn(out[k], w);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+template <int TX, int TY, int K>
+struct TiledShape {
+    static constexpr int NT = TX * TY / 4;     // threads per CTA
+    static constexpr int TXV = TX / 4;         // threads per tile row
+    static constexpr int RS = TX + 16;         // staged row: x0-8 .. x0+TX+7 (16B aligned)
+    static constexpr int ROWS = TY + 10;       // y0-5 .. y0+TY+4
+    static constexpr int BOX_FLOATS = RS * ROWS;
+    static constexpr int SLOT = (BOX_FLOATS + 31) / 32 * 32;  // 128-byte aligned slots
+    static constexpr uint32_t BOX_BYTES = BOX_FLOATS * 4;
+    static constexpr size_t SMEM = size_t(K) * SLOT * 4 + size_t(K) * 8;
+    static_assert(TX % 4 == 0 && RS <= 256 && ROWS <= 256, "TMA box limits");
+    static_assert(K >= 10, "ring must hold the 10 prologue planes");
+};
+
+template <int TX, int TY, int K, int MINB>
+__global__ void __launch_bounds__(TX * TY / 4, MINB)
+    k_tiled(const __grid_constant__ CUtensorMap tm, const __grid_constant__ StencilParams p) {
+    using S = TiledShape<TX, TY, K>;
+    extern __shared__ __align__(128) float smem[];
+    float* ring = smem;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + K * S::SLOT);
+
+    const int tid = threadIdx.x;
+    const int tx = tid % S::TXV, ty = tid / S::TXV;
+
+    // ---- work unit: (z-chunk, tile), chunk-major so concurrently running CTAs are xy
+    // neighbours at similar z (their halo re-reads hit L2)
+    const int ntiles = p.tiles_x * p.tiles_y;
+    int chunk = blockIdx.x / ntiles;
+    const int tile = blockIdx.x - chunk * ntiles;
+    int r = 0;
+    if (chunk >= p.r_chunks[0]) {
+        r = 1;
+        chunk -= p.r_chunks[0];
+    }
+    const int zs = p.r_begin[r] + static_cast<int>((long long)chunk * p.r_len[r] / p.r_chunks[r]);
+    const int ze = p.r_begin[r] + static_cast<int>((long long)(chunk + 1) * p.r_len[r] / p.r_chunks[r]);
+    const int tyi = tile / p.tiles_x;
+    const int x0 = (tile - tyi * p.tiles_x) * TX;
+    const int y0 = tyi * TY;
+    const int x = x0 + 4 * tx;
+    const int y = y0 + ty;
+    const bool active = (x < p.nx) && (y < p.ny);
+
+    if (tid == 0) {
+#pragma unroll 1
+        for (int k = 0; k < K; ++k) mbar_init(&bars[k], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    // plane j of this unit = owned plane zs-5+j = buffer plane zs+j
+    const int L = ze - zs + 10;
+    auto issue = [&](int j) {
+        const int slot = j % K;
+        mbar_expect_tx(&bars[slot], S::BOX_BYTES);
+        tma_load_3d(ring + slot * S::SLOT, &tm, x0 - 8, y0 - 5, zs + j, &bars[slot]);
+    };
+    if (tid == 0) {
+        const int first = L < K ? L : K;
+#pragma unroll 1
+        for (int j = 0; j < first; ++j) issue(j);
+    }
+
+    // sources in this thread's column within the unit (registration order = bit order)
+    uint64_t smask = 0;
+    if (active) {
+#pragma unroll 1
+        for (int s = 0; s < p.nsrc; ++s) {
+            const DevSource& src = p.src[s];
+            if (src.y == y && src.x >= x && src.x < x + 4 && src.z >= zs && src.z < ze)
+                smask |= (1ull << s);
+        }
+    }
+    if (p.write_next && blockIdx.x == 0 && tid == 0)
+        p.d_step[p.parity ^ 1] = p.d_step[p.parity] + 1;
+
+    const int own = (5 + ty) * S::RS + 8 + 4 * tx;
+    const long long col = (long long)y * p.nx + x;
+
+    // ---- prologue: queue <- planes zs-5 .. zs+4
+    float4 q[11];
+#pragma unroll
+    for (int j = 0; j < 10; ++j) {
+        mbar_wait(&bars[j % K], (j / K) & 1);
+        q[j] = *reinterpret_cast<const float4*>(ring + (j % K) * S::SLOT + own);
+    }
+    __syncthreads();  // planes zs-5 .. zs-1 fully consumed
+    if (tid == 0) {
+        fence_proxy_async();
+#pragma unroll 1
+        for (int j = 0; j < 5; ++j)
+            if (j + K < L) issue(j + K);
+    }
+
+    float4 upv = make_float4(0.f, 0.f, 0.f, 0.f), cv = upv;
+    if (active) {
+        upv = ld_stream4(p.next + (long long)(zs + 5) * p.plane + col);
+        cv = ld_stream4(p.C + (long long)zs * p.plane + col);
+    }
+    const float c[6] = {p.coef[0], p.coef[1], p.coef[2], p.coef[3], p.coef[4], p.coef[5]};
+
+#pragma unroll 1
+    for (int z = zs; z < ze; ++z) {
+        const int i = z - zs;
+        float4 upn = upv, cn = cv;
+        if (active && z + 1 < ze) {  // one plane ahead
+            upn = ld_stream4(p.next + (long long)(z + 6) * p.plane + col);
+            cn = ld_stream4(p.C + (long long)(z + 1) * p.plane + col);
+        }
+        const int jn = i + 10, jc = i + 5;
+        mbar_wait(&bars[jn % K], (jn / K) & 1);
+        q[10] = *reinterpret_cast<const float4*>(ring + (jn % K) * S::SLOT + own);
+
+        const float* row = ring + (jc % K) * S::SLOT + own;
+        float xs[14];
+        {
+            const float4 l = *reinterpret_cast<const float4*>(row - 4);
+            const float4 rr = *reinterpret_cast<const float4*>(row + 4);
+            xs[0] = row[-5];
+            xs[1] = l.x; xs[2] = l.y; xs[3] = l.z; xs[4] = l.w;
+            xs[5] = q[5].x; xs[6] = q[5].y; xs[7] = q[5].z; xs[8] = q[5].w;
+            xs[9] = rr.x; xs[10] = rr.y; xs[11] = rr.z; xs[12] = rr.w;
+            xs[13] = row[8];
+        }
+        float4 yv[11];
+#pragma unroll
+        for (int m = 1; m <= 5; ++m) {
+            yv[5 - m] = *reinterpret_cast<const float4*>(row - m * S::RS);
+            yv[5 + m] = *reinterpret_cast<const float4*>(row + m * S::RS);
+        }
+        yv[5] = q[5];
+
+        float out[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            float zl[11], yl[11], xl[11];
+#pragma unroll
+            for (int o = 0; o < 11; ++o) {
+                zl[o] = comp(q[o], k);
+                yl[o] = comp(yv[o], k);
+                xl[o] = xs[k + o];
+            }
+            out[k] = rtm_point(zl, yl, xl, comp(upv, k), comp(cv, k), c);
+        }
+        if (smask) add_sources(p, smask, x, z, out);
+        if (active)
+            st_stream4(p.next + (long long)(z + 5) * p.plane + col,
+                       make_float4(out[0], out[1], out[2], out[3]));
+
+#pragma unroll
+        for (int o = 0; o < 10; ++o) q[o] = q[o + 1];
+        upv = upn;
+        cv = cn;
+        __syncthreads();  // plane jc fully consumed -> its slot takes plane jc + K
+        if (tid == 0 && jc + K < L) {
+            fence_proxy_async();
+            issue(jc + K);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_naive(const __grid_constant__ StencilParams p) {
+    long long total = (long long)p.r_len[0] * p.plane;
+    if (p.nranges > 1) total += (long long)p.r_len[1] * p.plane;
+    if (p.write_next && blockIdx.x == 0 && threadIdx.x == 0)
+        p.d_step[p.parity ^ 1] = p.d_step[p.parity] + 1;
+    const float c[6] = {p.coef[0], p.coef[1], p.coef[2], p.coef[3], p.coef[4], p.coef[5]};
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        long long tt = t;
+        int z;
+        const long long n0 = (long long)p.r_len[0] * p.plane;
+        if (tt < n0) {
+            z = p.r_begin[0] + static_cast<int>(tt / p.plane);
+        } else {
+            tt -= n0;
+            z = p.r_begin[1] + static_cast<int>(tt / p.plane);
+        }
+        const long long inplane = tt % p.plane;
+        const int y = static_cast<int>(inplane / p.nx);
+        const int x = static_cast<int>(inplane - (long long)y * p.nx);
+        const long long pb = (long long)(z + 5) * p.plane + inplane;  // buffer index
+        float zl[11], yl[11], xl[11];
+#pragma unroll
+        for (int o = -5; o <= 5; ++o) {
+            zl[o + 5] = p.u[pb + o * p.plane];  // z-halo planes are explicit
+            const int yy = y + o, xx = x + o;
+            yl[o + 5] = (yy >= 0 && yy < p.ny) ? p.u[pb + (long long)o * p.nx] : 0.0f;
+            xl[o + 5] = (xx >= 0 && xx < p.nx) ? p.u[pb + o] : 0.0f;
+        }
+        float out = rtm_point(zl, yl, xl, p.next[pb], p.C[(long long)z * p.plane + inplane], c);
+        for (int s = 0; s < p.nsrc; ++s) {
+            const DevSource& src = p.src[s];
+            if (src.x == x && src.y == y && src.z == z) {
+                const int n = p.d_step[p.parity];
+                if (n < src.nsamples) out = __fadd_rn(out, p.samples[src.offset + n]);
+            }
+        }
+        p.next[pb] = out;
+    }
+}
+
+// ------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_velocity(const float* v, float* C, long long n, double dt,
+                                                  double dx, unsigned int* stats) {
+    float vmax = 0.0f;
+    unsigned int bad = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float vi = v[i];
+        if (!(isfinite(vi) && vi > 0.0f)) {
+            ++bad;
+        } else {
+            vmax = fmaxf(vmax, vi);
+        }
+        // (double(v) * double(dt)) / double(dx), squared, rounded once to fp32 (a1)
+        const double nu = __ddiv_rn(__dmul_rn(static_cast<double>(vi), dt), dx);
+        C[i] = __double2float_rn(__dmul_rn(nu, nu));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+        bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&stats[0], __float_as_uint(vmax));  // v > 0: uint order == float order
+        if (bad) atomicAdd(&stats[1], bad);
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// Variant table.  id 0 = naive.
+#define RTM_TILED_VARIANTS(X)            \
+    X(1, "tma64x16k10", 64, 16, 10, 2)   \
+    X(2, "tma32x16k10", 32, 16, 10, 3)   \
+    X(3, "tma64x8k10", 64, 8, 10, 3)     \
+    X(4, "tma128x8k10", 128, 8, 10, 2)   \
+    X(5, "tma32x32k10", 32, 32, 10, 2)   \
+    X(6, "tma64x16k12", 64, 16, 12, 2)   \
+    X(7, "tma128x16k10", 128, 16, 10, 1) \
+    X(8, "tma64x32k10", 64, 32, 10, 1)   \
+    X(9, "tma32x8k10", 32, 8, 10, 4)
+
+static const TileVariant kVariants[] = {
+    {"naive", 0, 0, 0, 0},
+#define X(id, name, tx, ty, k, mb) {name, tx, ty, k, mb},
+    RTM_TILED_VARIANTS(X)
+#undef X
+};
+
+int num_variants() { return static_cast<int>(sizeof(kVariants) / sizeof(kVariants[0])); }
+const TileVariant& variant(int id) { return kVariants[id]; }
+
+size_t tiled_smem_bytes(int id) {
+    switch (id) {
+#define X(vid, name, tx, ty, k, mb) \
+    case vid:                       \
+        return TiledShape<tx, ty, k>::SMEM;
+        RTM_TILED_VARIANTS(X)
+#undef X
+        default:
+            return 0;
+    }
+}
+
+template <int TX, int TY, int K, int MINB>
+static cudaError_t prepare(const void** fn, int* threads, size_t* smem) {
+    using S = TiledShape<TX, TY, K>;
+    *fn = reinterpret_cast<const void*>(&k_tiled<TX, TY, K, MINB>);
+    *threads = S::NT;
+    *smem = S::SMEM;
+    return cudaFuncSetAttribute(&k_tiled<TX, TY, K, MINB>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(S::SMEM));
+}
+
+static cudaError_t variant_fn(int id, const void** fn, int* threads, size_t* smem) {
+    switch (id) {
+#define X(vid, name, tx, ty, k, mb) \
+    case vid:                       \
+        return prepare<tx, ty, k, mb>(fn, threads, smem);
+        RTM_TILED_VARIANTS(X)
+#undef X
+        default:
+            return cudaErrorInvalidValue;
+    }
+}
+
+int tiled_occupancy(int id, int* threads_per_block) {
+    const void* fn;
+    int threads;
+    size_t smem;
+    if (variant_fn(id, &fn, &threads, &smem) != cudaSuccess) return -1;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem) != cudaSuccess)
+        return -1;
+    if (threads_per_block) *threads_per_block = threads;
+    return nb;
+}
+
+cudaError_t launch_tiled(int id, const CUtensorMap& tm, const StencilParams& p, cudaStream_t s) {
+    const void* fn;
+    int threads;
+    size_t smem;
+    cudaError_t e = variant_fn(id, &fn, &threads, &smem);
+    if (e != cudaSuccess) return e;
+    const long long units = (long long)p.tiles_x * p.tiles_y *
+                            (p.r_chunks[0] + (p.nranges > 1 ? p.r_chunks[1] : 0));
+    if (units <= 0) return cudaSuccess;
+    void* args[] = {const_cast<CUtensorMap*>(&tm), const_cast<StencilParams*>(&p)};
+    return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(units)), dim3(threads), args, smem, s);
+}
+
+cudaError_t launch_naive(const StencilParams& p, cudaStream_t s) {
+    long long total = (long long)p.r_len[0] * p.plane;
+    if (p.nranges > 1) total += (long long)p.r_len[1] * p.plane;
+    if (total <= 0) return cudaSuccess;
+    long long blocks = (total + 255) / 256;
+    if (blocks > 148LL * 64) blocks = 148LL * 64;
+    k_naive<<<static_cast<unsigned>(blocks), 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_velocity(const float* v, float* C, long long n, double dt, double dx,
+                            unsigned int* stats, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    long long blocks = (n + 255) / 256;
+    if (blocks > 148LL * 16) blocks = 148LL * 16;
+    k_velocity<<<static_cast<unsigned>(blocks), 256, 0, s>>>(v, C, n, dt, dx, stats);
+    return cudaGetLastError();
+}
+
+}  // namespace rtm

@@ -1,0 +1,254 @@
+"""Thin ctypes binding of the C ABI in include/rtm.h (argument marshalling only).
+
+Every function here has the name of the C entry point it calls.  Arrays are numpy
+float32, C-contiguous, shape (nz, ny, nx) (x fastest), or raw device pointers (ints, e.g.
+``tensor.data_ptr()``) for the ``*_device`` calls.  Errors raise :class:`RtmError` with
+the library's rtm_last_error() message.  There is no fallback: if ``librtm_b200.so`` is
+missing or cannot be loaded, importing this module fails.
+"""
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+import numpy as np
+
+_LIB_PATH = Path(__file__).resolve().parent / "librtm_b200.so"
+
+RTM_OK, RTM_EINVAL, RTM_ECFL, RTM_ENOMEM, RTM_ECUDA, RTM_ENCCL, RTM_ESTATE = 0, -1, -2, -3, -4, -5, -6
+RTM_MAX_SOURCES = 64
+_NAMES = {0: "RTM_OK", -1: "RTM_EINVAL", -2: "RTM_ECFL", -3: "RTM_ENOMEM", -4: "RTM_ECUDA",
+          -5: "RTM_ENCCL", -6: "RTM_ESTATE"}
+
+
+class RtmError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+if not _LIB_PATH.exists():
+    raise ImportError(f"{_LIB_PATH} not built; run python -m paper_1310_8232_b200.build "
+                      "(the product has no CPU fallback)")
+lib = ctypes.CDLL(str(_LIB_PATH))
+
+_P, _I, _F, _D, _LL = ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.c_double, ctypes.c_longlong
+_SIGS = {
+    "rtm_create": (_P, [_I, _I, _I, _F, _F, _P]),
+    "rtm_set_velocity": (_I, [_P, _P]),
+    "rtm_inject_source": (_I, [_P, _I, _I, _I, _P, _I]),
+    "rtm_step": (_I, [_P, _I]),
+    "rtm_read_field": (_I, [_P, _P]),
+    "rtm_destroy": (None, [_P]),
+    "rtm_last_error": (ctypes.c_char_p, []),
+    "rtm_set_fields": (_I, [_P, _P, _P]),
+    "rtm_read_fields": (_I, [_P, _P, _P]),
+    "rtm_reset": (_I, [_P]),
+    "rtm_step_count": (_LL, [_P]),
+    "rtm_set_velocity_device": (_I, [_P, _P]),
+    "rtm_read_field_device": (_I, [_P, _P]),
+    "rtm_set_tile": (_I, [_P, _I]),
+    "rtm_get_tile": (_I, [_P]),
+    "rtm_num_tiles": (_I, []),
+    "rtm_set_zchunk": (_I, [_P, _I]),
+    "rtm_tile_name": (ctypes.c_char_p, [_I]),
+    "rtm_set_stream": (_I, [_P, _P]),
+    "rtm_last_elapsed_ms": (_F, [_P]),
+    "rtm_set_profiling": (_I, [_P, _I]),
+    "rtm_kernel_stats": (_I, [_P, ctypes.POINTER(_LL), ctypes.POINTER(_D)]),
+    "rtm_launch_count": (_LL, [_P]),
+    "rtm_create_multi": (_P, [_I, _I, _I, _F, _F, _P, _I, _P]),
+    "rtm_get_unique_id": (_I, [_P]),
+    "rtm_create_dist": (_P, [_I, _I, _I, _F, _F, _P, _I, _I, _P, _I]),
+    "rtm_slab_range": (_I, [_I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
+    "rtm_halo_plan": (_I, [_I, _I, _I, _I, _I, ctypes.POINTER(_LL), ctypes.POINTER(_LL)]),
+    "rtm_nu_crit": (_D, [_P]),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+def _err() -> str:
+    m = lib.rtm_last_error()
+    return m.decode() if m else ""
+
+
+def _check(rc: int) -> int:
+    if rc != RTM_OK:
+        raise RtmError(rc, _err())
+    return rc
+
+
+def _f32(a, n=None, name="array"):
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    if n is not None and a.size != n:
+        raise ValueError(f"{name} has {a.size} elements, expected {n}")
+    return a
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(_P)
+
+
+def _coeffs(c):
+    c = np.ascontiguousarray(c, dtype=np.float32)
+    if c.size != 6:
+        raise ValueError("coeffs must have 6 entries c0..c5")
+    return c
+
+
+# ---- north-star entry points ------------------------------------------------------------
+def rtm_create(nx, ny, nz, dx, dt, coeffs):
+    c = _coeffs(coeffs)
+    h = lib.rtm_create(int(nx), int(ny), int(nz), float(dx), float(dt), _ptr(c))
+    if not h:
+        raise RtmError(RTM_EINVAL if "CUDA" not in _err() else RTM_ECUDA, _err())
+    return h
+
+
+def rtm_set_velocity(h, v, n=None):
+    v = _f32(v, n, "v")
+    return _check(lib.rtm_set_velocity(h, _ptr(v)))
+
+
+def rtm_inject_source(h, ix, iy, iz, samples):
+    s = _f32(samples)
+    return _check(lib.rtm_inject_source(h, int(ix), int(iy), int(iz), _ptr(s) if s.size else None,
+                                        int(s.size)))
+
+
+def rtm_step(h, nsteps):
+    return _check(lib.rtm_step(h, int(nsteps)))
+
+
+def rtm_read_field(h, out):
+    assert out.dtype == np.float32 and out.flags.c_contiguous
+    return _check(lib.rtm_read_field(h, _ptr(out)))
+
+
+def rtm_destroy(h):
+    if h:
+        lib.rtm_destroy(h)
+
+
+def rtm_last_error() -> str:
+    return _err()
+
+
+# ---- extensions --------------------------------------------------------------------------
+def rtm_set_fields(h, u=None, u_prev=None):
+    u = None if u is None else _f32(u)
+    up = None if u_prev is None else _f32(u_prev)
+    return _check(lib.rtm_set_fields(h, _ptr(u), _ptr(up)))
+
+
+def rtm_read_fields(h, u=None, u_prev=None):
+    return _check(lib.rtm_read_fields(h, _ptr(u), _ptr(u_prev)))
+
+
+def rtm_reset(h):
+    return _check(lib.rtm_reset(h))
+
+
+def rtm_step_count(h) -> int:
+    return int(lib.rtm_step_count(h))
+
+
+def rtm_set_velocity_device(h, dptr: int):
+    return _check(lib.rtm_set_velocity_device(h, _P(int(dptr))))
+
+
+def rtm_read_field_device(h, dptr: int):
+    return _check(lib.rtm_read_field_device(h, _P(int(dptr))))
+
+
+def rtm_set_tile(h, tile_id):
+    return _check(lib.rtm_set_tile(h, int(tile_id)))
+
+
+def rtm_get_tile(h) -> int:
+    return int(lib.rtm_get_tile(h))
+
+
+def rtm_num_tiles() -> int:
+    return int(lib.rtm_num_tiles())
+
+
+def rtm_tile_name(tile_id) -> str | None:
+    n = lib.rtm_tile_name(int(tile_id))
+    return n.decode() if n else None
+
+
+def rtm_set_zchunk(h, planes):
+    return _check(lib.rtm_set_zchunk(h, int(planes)))
+
+
+def rtm_set_stream(h, stream_handle):
+    return _check(lib.rtm_set_stream(h, _P(int(stream_handle)) if stream_handle else None))
+
+
+def rtm_last_elapsed_ms(h) -> float:
+    return float(lib.rtm_last_elapsed_ms(h))
+
+
+def rtm_set_profiling(h, on):
+    return _check(lib.rtm_set_profiling(h, int(bool(on))))
+
+
+def rtm_kernel_stats(h):
+    n, ms = _LL(0), _D(0)
+    _check(lib.rtm_kernel_stats(h, ctypes.byref(n), ctypes.byref(ms)))
+    return int(n.value), float(ms.value)
+
+
+def rtm_launch_count(h) -> int:
+    return int(lib.rtm_launch_count(h))
+
+
+def rtm_create_multi(nx, ny, nz, dx, dt, coeffs, devices):
+    c = _coeffs(coeffs)
+    d = np.ascontiguousarray(devices, dtype=np.int32)
+    h = lib.rtm_create_multi(int(nx), int(ny), int(nz), float(dx), float(dt), _ptr(c), int(d.size),
+                             _ptr(d))
+    if not h:
+        raise RtmError(RTM_EINVAL, _err())
+    return h
+
+
+def rtm_get_unique_id() -> bytes:
+    buf = (ctypes.c_ubyte * 128)()
+    _check(lib.rtm_get_unique_id(ctypes.cast(buf, _P)))
+    return bytes(buf)
+
+
+def rtm_create_dist(nx, ny, nz_global, dx, dt, coeffs, rank, world, uid: bytes, device):
+    c = _coeffs(coeffs)
+    if len(uid) != 128:
+        raise ValueError("unique id must be 128 bytes")
+    buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)
+    h = lib.rtm_create_dist(int(nx), int(ny), int(nz_global), float(dx), float(dt), _ptr(c),
+                            int(rank), int(world), ctypes.cast(buf, _P), int(device))
+    if not h:
+        raise RtmError(RTM_ENCCL if "NCCL" in _err() else RTM_EINVAL, _err())
+    return h
+
+
+def rtm_slab_range(nz_global, world, rank):
+    z0, nzl = _I(0), _I(0)
+    _check(lib.rtm_slab_range(int(nz_global), int(world), int(rank), ctypes.byref(z0),
+                              ctypes.byref(nzl)))
+    return int(z0.value), int(nzl.value)
+
+
+def rtm_halo_plan(nx, ny, nzl, rank, world):
+    offs = (_LL * 4)()
+    cnt = _LL(0)
+    _check(lib.rtm_halo_plan(int(nx), int(ny), int(nzl), int(rank), int(world), offs,
+                             ctypes.byref(cnt)))
+    return [int(o) for o in offs], int(cnt.value)
+
+
+def rtm_nu_crit(coeffs) -> float:
+    return float(lib.rtm_nu_crit(_ptr(_coeffs(coeffs))))

@@ -64,9 +64,13 @@ def source_samples(v_s: float, dt: float, f0: float, nsteps: int) -> np.ndarray:
 def random_fields(shape, seed: int = 0, scale: float = 1.0):
     """Seeded U[-scale, scale] initial conditions (u, u_prev), fp32."""
     g = np.random.default_rng([SEED_BASE, 1000, int(seed)])
-    u = g.uniform(-scale, scale, size=shape).astype(np.float32)
-    up = g.uniform(-scale, scale, size=shape).astype(np.float32)
-    return u, up
+    out = []
+    for _ in range(2):  # float32 draws (no float64 temporaries at 1024^3)
+        a = g.random(size=shape, dtype=np.float32)
+        a *= np.float32(2 * scale)
+        a -= np.float32(scale)
+        out.append(a)
+    return out[0], out[1]
 
 
 # ---------------------------------------------------------------------------------------
@@ -124,8 +128,21 @@ class SmoothNoise:
         self.g = gaussian_filter(g, sigma=1.0, mode="reflect", truncate=4.0).astype(np.float32)
         self._gxy = _lerp_axis(_lerp_axis(self.g, 2, nx, self.L), 1, ny, self.L)
 
-    def planes(self, z0: int, z1: int) -> np.ndarray:
-        return _lerp_axis(self._gxy, 0, z1 - z0, self.L, offset=z0).astype(np.float32)
+    def planes(self, z0: int, z1: int, out: np.ndarray | None = None) -> np.ndarray:
+        """Fine planes z0..z1-1 (linear interpolation along z, plane by plane)."""
+        nz, ny, nx = self.shape
+        if out is None:
+            out = np.empty((z1 - z0, ny, nx), np.float32)
+        tmp = np.empty((ny, nx), np.float32)
+        for z in range(z0, z1):
+            i0 = z // self.L
+            f = np.float32((z - i0 * self.L) / self.L)
+            o = out[z - z0]
+            np.multiply(self._gxy[i0], np.float32(1.0) - f, out=o)
+            if f != 0:
+                np.multiply(self._gxy[i0 + 1], f, out=tmp)
+                o += tmp
+        return out
 
     def full(self, chunk: int = 64) -> np.ndarray:
         nz, ny, nx = self.shape
@@ -170,9 +187,10 @@ def layered_smooth_velocity(rng, shape, dx, dt, sigma=8, amp=300.0):
     # std over the whole field, two passes, chunked
     s1 = s2 = 0.0
     for z0 in range(0, nz, chunk):
-        p = sn.planes(z0, min(nz, z0 + chunk)).astype(np.float64)
-        s1 += p.sum()
-        s2 += (p * p).sum()
+        p = sn.planes(z0, min(nz, z0 + chunk))
+        for q in p.reshape(p.shape[0], -1):
+            s1 += float(q.sum(dtype=np.float64))
+            s2 += float(np.dot(q, q))
     n = float(nz) * ny * nx
     std = math.sqrt(max(s2 / n - (s1 / n) ** 2, 1e-30))
     lz = (len(layers) * np.arange(nz)) // nz

@@ -1,0 +1,122 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every symbol include/rtm.h
+declares, its host-only helpers are right, and it fails loudly without a GPU."""
+from __future__ import annotations
+
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import rtm_inputs as ri
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_1310_8232_b200 import build
+    build.build()
+    import paper_1310_8232_b200 as P
+    return P
+
+
+def declared_functions():
+    text = (ROOT / "include" / "rtm.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(rtm_[a-z_]+)\s*\(", text)))
+
+
+def test_header_declares_north_star_calls():
+    names = declared_functions()
+    for n in ("rtm_create", "rtm_set_velocity", "rtm_inject_source", "rtm_step", "rtm_read_field"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(P):
+    import ctypes
+    lib = ctypes.CDLL(str(ROOT / "paper_1310_8232_b200" / "librtm_b200.so"))
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+    # and the binding wraps each one under the same name
+    assert not [n for n in declared_functions() if not hasattr(P, n)]
+
+
+def test_no_cpu_fallback_without_gpu(P):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(P.RtmError) as e:
+        P.rtm_create(64, 64, 64, 10.0, 1e-3, ri.COEFFS_F32)
+    assert "no CUDA device" in str(e.value)
+
+
+def test_argument_validation_before_device(P):
+    for args in [(0, 4, 4, 10.0, 1e-3), (4, 4, 4, -1.0, 1e-3), (4, 4, 4, 10.0, float("nan"))]:
+        with pytest.raises(P.RtmError) as e:
+            P.rtm_create(*args, ri.COEFFS_F32)
+        assert e.value.code == P.RTM_EINVAL
+    bad = ri.COEFFS_F32.copy()
+    bad[1] = -bad[1]  # not a negative-definite second difference
+    with pytest.raises(P.RtmError):
+        P.rtm_create(8, 8, 8, 10.0, 1e-3, bad)
+
+
+def test_nu_crit_closed_form(P):
+    # 3D leapfrog bound 2/sqrt(3 S(pi)), S(pi) = 512/75 -> 5/sqrt(128)
+    assert P.rtm_nu_crit(ri.COEFFS_F32) == pytest.approx(5 / np.sqrt(128), rel=1e-7)
+    # second-order coefficients (-2, 1, 0...): S_max = 4 -> nu_crit = 1/sqrt(3)
+    c2 = np.array([-2, 1, 0, 0, 0, 0], np.float32)
+    assert P.rtm_nu_crit(c2) == pytest.approx(1 / np.sqrt(3), rel=1e-9)
+
+
+@pytest.mark.parametrize("nz,world", [(1024, 8), (512, 2), (101, 3), (20, 2), (7, 1)])
+def test_slab_range_partitions_exactly(P, nz, world):
+    spans = [P.rtm_slab_range(nz, world, r) for r in range(world)]
+    assert spans[0][0] == 0
+    for (a, n), (b, _) in zip(spans, spans[1:]):
+        assert a + n == b
+    assert spans[-1][0] + spans[-1][1] == nz
+    assert max(n for _, n in spans) - min(n for _, n in spans) <= 1
+
+
+def test_slab_range_rejects_thin_slabs(P):
+    with pytest.raises(P.RtmError):
+        P.rtm_slab_range(19, 2, 0)
+    with pytest.raises(P.RtmError):
+        P.rtm_slab_range(64, 2, 2)
+
+
+def test_halo_plan_layout(P):
+    nx, ny, nzl = 8, 6, 12
+    plane = nx * ny
+    offs, cnt = P.rtm_halo_plan(nx, ny, nzl, 1, 3)
+    assert cnt == 5 * plane
+    assert offs == [5 * plane, 0, nzl * plane, (nzl + 5) * plane]
+    offs0, _ = P.rtm_halo_plan(nx, ny, nzl, 0, 3)
+    assert offs0[:2] == [-1, -1] and offs0[2] >= 0
+    offs2, _ = P.rtm_halo_plan(nx, ny, nzl, 2, 3)
+    assert offs2[2:] == [-1, -1] and offs2[0] >= 0
+
+
+def test_tile_table(P):
+    n = P.rtm_num_tiles()
+    assert n >= 2 and P.rtm_tile_name(0) == "naive"
+    assert all(P.rtm_tile_name(i).startswith("tma") for i in range(1, n))
+    assert P.rtm_tile_name(n) is None and P.rtm_tile_name(-5) is None
+
+
+def test_sass_has_tma_and_no_legacy_tensor_ops():
+    """The tiled kernels use TMA (UTMALDG) and mbarrier sync; the path is not a GEMM, so no
+    HMMA/UTC*MMA (BASELINE.json north_star: no tensor cores)."""
+    import shutil
+    import subprocess
+    so = ROOT / "paper_1310_8232_b200" / "librtm_b200.so"
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not Path(cuobjdump).exists():
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([cuobjdump, "-sass", str(so)], capture_output=True, text=True).stdout
+    assert "sm_100a" in sass or "SM100" in sass.upper()
+    assert "UTMALDG" in sass
+    assert "SYNCS" in sass  # mbarrier operations
+    assert "HMMA" not in sass

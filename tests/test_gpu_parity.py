@@ -1,0 +1,374 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element, on
+the same seeded inputs (BASELINE.json north_star tolerances: max|d| <= 1e-5 max|u| after one
+step, <= 1e-4 max|u| after the config's full step count).  Plus bitwise identity across all
+kernel variants and slab decompositions, ABI properties and errors."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import rtm_inputs as ri
+
+pytestmark = pytest.mark.gpu
+
+TOL_1 = 1e-5
+TOL_FULL = 1e-4
+C32 = ri.COEFFS_F32
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_1310_8232_b200 import build
+    build.build()
+    import paper_1310_8232_b200 as P
+    return P
+
+
+def relerr(a, b):
+    m = float(np.abs(b).max())
+    return float(np.abs(a.astype(np.float64) - b).max()) / (m if m > 0 else 1.0)
+
+
+def gpu_run(P, v, dx, dt, steps, u0=None, up0=None, sources=(), tile=-1, devices=None):
+    nz, ny, nx = v.shape
+    with P.Simulation(nx, ny, nz, dx, dt, C32, devices=devices) as sim:
+        if tile != -1:
+            sim.set_tile(tile)
+        sim.set_velocity(v)
+        for (x, y, z, w) in sources:
+            sim.inject_source(x, y, z, w)
+        if u0 is not None or up0 is not None:
+            sim.set_fields(u0, up0)
+        sim.step(steps)
+        assert sim.steps_taken == steps
+        return sim.read_field()
+
+
+# ----------------------------------------------------------------------------- configs
+def test_c1_full_run_vs_oracle(P):
+    cfg = ri.make_config(1)
+    v = cfg.velocity()
+    src = cfg.sources()
+    ref = oracle.run(v, cfg.dx, cfg.dt, C32, cfg.steps, sources=src)
+    got = gpu_run(P, v, cfg.dx, cfg.dt, cfg.steps, sources=src)
+    assert relerr(got, ref) <= TOL_FULL
+    assert np.abs(ref).max() > 0
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_one_step_random_ics_small_grids(P, k):
+    """1 step from seeded U[-1,1] ICs on each config's velocity recipe, at a size the oracle
+    finishes in well under a second, spanning several tiles with ragged x/y/z tails."""
+    cfg = ri.make_config(k, shape=(45, 70, 136), steps=1)
+    v = cfg.velocity()
+    u0, up0 = ri.random_fields(v.shape, seed=k)
+    src = cfg.sources()
+    ref = oracle.run(v, cfg.dx, cfg.dt, C32, 1, u0=u0, up0=up0, sources=src)
+    got = gpu_run(P, v, cfg.dx, cfg.dt, 1, u0=u0, up0=up0, sources=src)
+    assert relerr(got, ref) <= TOL_1
+
+
+def test_c2_full_run_vs_oracle(P):
+    cfg = ri.make_config(2)
+    v = cfg.velocity()
+    src = cfg.sources()
+    ref = oracle.run(v, cfg.dx, cfg.dt, C32, cfg.steps, sources=src)
+    got = gpu_run(P, v, cfg.dx, cfg.dt, cfg.steps, sources=src)
+    assert relerr(got, ref) <= TOL_FULL
+
+
+def test_c2_one_step_random_ics(P):
+    cfg = ri.make_config(2)
+    v = cfg.velocity()
+    u0, up0 = ri.random_fields(v.shape, seed=22)
+    ref = oracle.run(v, cfg.dx, cfg.dt, C32, 1, u0=u0, up0=up0, sources=cfg.sources())
+    got = gpu_run(P, v, cfg.dx, cfg.dt, 1, u0=u0, up0=up0, sources=cfg.sources())
+    assert relerr(got, ref) <= TOL_1
+
+
+def test_c3_full_grid_20_steps_vs_oracle(P):
+    cfg = ri.make_config(3, steps=20)
+    v = cfg.velocity()
+    u0, up0 = ri.random_fields(v.shape, seed=33)
+    src = cfg.sources()
+    ref = oracle.run(v, cfg.dx, cfg.dt, C32, 20, u0=u0, up0=up0, sources=src)
+    got = gpu_run(P, v, cfg.dx, cfg.dt, 20, u0=u0, up0=up0, sources=src)
+    assert relerr(got, ref) <= TOL_FULL
+
+
+@pytest.mark.parametrize("k", [4, 5])
+def test_full_size_one_step_sampled(P, k):
+    """Full BASELINE sizes (C4 1024^3, C5 1024x1024x256), in the bench's launch config:
+    one step from random ICs, 200k sampled points + all of a few boundary lines checked
+    one by one against the oracle's point evaluator."""
+    cfg = ri.make_config(k)
+    v = cfg.velocity()
+    u0, up0 = ri.random_fields(v.shape, seed=40 + k)
+    got = gpu_run(P, v, cfg.dx, cfg.dt, 1, u0=u0, up0=up0)
+    nz, ny, nx = v.shape
+    rng = np.random.default_rng(k)
+    pts = np.stack([rng.integers(0, nx, 200_000), rng.integers(0, ny, 200_000),
+                    rng.integers(0, nz, 200_000)], 1)
+    edges = []
+    for z in (0, 1, 4, 5, nz // 2, nz - 5, nz - 1):
+        for y in (0, 4, ny - 1):
+            edges.append(np.stack([np.arange(nx), np.full(nx, y), np.full(nx, z)], 1))
+    pts = np.concatenate([pts] + edges).astype(np.int32)
+    ref = oracle.points_f32(v, cfg.dx, cfg.dt, C32, u0, up0, pts)
+    g = got[pts[:, 2], pts[:, 1], pts[:, 0]]
+    assert relerr(g, ref) <= TOL_1
+
+
+# ----------------------------------------------------------------------------- variants
+def test_all_variants_bitwise_identical_and_match_oracle(P):
+    """Every tile variant (and the naive kernel) computes the same bits: one per-point
+    expression (SPEC.md:83 tiling transparency).  Ragged in x, y and z."""
+    nz, ny, nx = 29, 37, 100
+    rng = np.random.default_rng(5)
+    v = rng.uniform(1500, 4300, (nz, ny, nx)).astype(np.float32)
+    u0, up0 = ri.random_fields(v.shape, seed=5)
+    w = ri.source_samples(3000.0, 1e-3, 15.0, 7)
+    src = [(3, 4, 5, w), (99, 36, 28, -w), (0, 0, 0, w), (50, 20, 14, 0.5 * w), (50, 20, 14, w)]
+    ref = oracle.run(v, 10.0, 1e-3, C32, 7, u0=u0, up0=up0, sources=src)
+    outs = [gpu_run(P, v, 10.0, 1e-3, 7, u0=u0, up0=up0, sources=src, tile=t)
+            for t in range(P.rtm_num_tiles())]
+    for t, o in enumerate(outs):
+        assert np.array_equal(o, outs[0]), P.rtm_tile_name(t)
+    assert relerr(outs[0], ref) <= TOL_1 * 10
+
+
+@pytest.mark.parametrize("zchunk", [1, 3, 8, 64])
+def test_zchunking_bitwise(P, zchunk):
+    nz, ny, nx = 40, 24, 64
+    v = np.full((nz, ny, nx), 2500.0, np.float32)
+    u0, up0 = ri.random_fields(v.shape, seed=9)
+    base = gpu_run(P, v, 10.0, 1e-3, 5, u0=u0, up0=up0, tile=1)
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32) as sim:
+        sim.set_tile(1)
+        P.rtm_set_zchunk(sim.h, zchunk)
+        sim.set_velocity(v)
+        sim.set_fields(u0, up0)
+        sim.step(5)
+        assert np.array_equal(sim.read_field(), base)
+
+
+def test_graph_and_direct_launch_paths_agree(P):
+    """rtm_step uses CUDA graphs for runs of >= 16 steps from an even step; stepping one at a
+    time (no graph) must give the same bits, including the source sample index."""
+    cfg = ri.make_config(1, steps=40)
+    v = cfg.velocity()
+    src = cfg.sources()
+    a = gpu_run(P, v, cfg.dx, cfg.dt, 40, sources=src)
+    with P.Simulation(64, 64, 64, cfg.dx, cfg.dt, C32) as sim:
+        sim.set_velocity(v)
+        for s in src:
+            sim.inject_source(*s)
+        for _ in range(3):
+            sim.step(1)           # odd start -> direct launches
+        sim.step(33)              # direct, then graph
+        sim.step(4)
+        assert np.array_equal(sim.read_field(), a)
+
+
+# ----------------------------------------------------------------------------- slabs
+@pytest.mark.parametrize("G", [2, 3, 4])
+def test_multislab_on_one_gpu_bitwise_equals_single(P, G):
+    """z-slab decomposition (boundary planes first, halo copies, interior) on one GPU gives
+    exactly the G=1 field (R14)."""
+    nz, ny, nx = 47, 33, 72
+    rng = np.random.default_rng(G)
+    v = rng.uniform(1500, 4300, (nz, ny, nx)).astype(np.float32)
+    u0, up0 = ri.random_fields(v.shape, seed=100 + G)
+    w = ri.source_samples(2500.0, 1e-3, 15.0, 9)
+    bounds = [P.rtm_slab_range(nz, G, r)[0] for r in range(1, G)]
+    src = [(5, 6, b, w) for b in bounds] + [(7, 8, b - 1, -w) for b in bounds] + [(1, 1, 0, w)]
+    ref = gpu_run(P, v, 10.0, 1e-3, 9, u0=u0, up0=up0, sources=src)
+    got = gpu_run(P, v, 10.0, 1e-3, 9, u0=u0, up0=up0, sources=src, devices=[0] * G)
+    assert np.array_equal(got, ref)
+    orc = oracle.run(v, 10.0, 1e-3, C32, 9, u0=u0, up0=up0, sources=src)
+    assert relerr(got, orc) <= TOL_1 * 10
+
+
+def test_dist_world1_equals_single(P):
+    nz, ny, nx = 20, 16, 32
+    v = np.full((nz, ny, nx), 2000.0, np.float32)
+    u0, up0 = ri.random_fields(v.shape, seed=3)
+    ref = gpu_run(P, v, 10.0, 1e-3, 6, u0=u0, up0=up0)
+    uid = P.rtm_get_unique_id()
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, dist=(0, 1, uid, 0)) as sim:
+        sim.set_velocity(v)
+        sim.set_fields(u0, up0)
+        sim.step(6)
+        assert np.array_equal(sim.read_field(), ref)
+
+
+# ----------------------------------------------------------------------------- properties
+def test_zero_fixed_point(P):
+    v = np.full((16, 12, 20), 3000.0, np.float32)
+    out = gpu_run(P, v, 10.0, 1e-3, 10, sources=[(3, 3, 3, np.zeros(10, np.float32))])
+    assert not np.any(out)
+
+
+def test_source_sample_timing(P):
+    """sample n is added right after the stencil of step n (R4)."""
+    v = np.full((12, 12, 12), 2000.0, np.float32)
+    w = np.array([0.5, 0.25, 2.0], np.float32)
+    out = gpu_run(P, v, 10.0, 1e-3, 1, sources=[(5, 6, 7, w)])
+    assert out[7, 6, 5] == w[0] and np.count_nonzero(out) == 1
+
+
+def test_mirror_symmetry_c1(P):
+    """Centred source on 64^3: u(32+k) = u(32-k) per axis for k <= 31 (the boundary-induced
+    asymmetry is ~1e-11 max|u| in fp64 over C1's 100 steps)."""
+    cfg = ri.make_config(1)
+    out = gpu_run(P, cfg.velocity(), cfg.dx, cfg.dt, cfg.steps, sources=cfg.sources())
+    m = np.abs(out).max()
+    s = out[1:, 1:, 1:]
+    for ax in range(3):
+        assert np.abs(s - np.flip(s, axis=ax)).max() <= 1e-6 * m
+
+
+def test_polynomial_laplacian_through_abi(P):
+    """u_prev = 2u trick: u^1 = C * L(u); for u = (x-xc)^a (y-yc)^b /h^(a+b) of per-axis
+    degree <= 10 the result is C * analytic Laplacian away from the boundary."""
+    nz, ny, nx = 24, 28, 32
+    h = 6.0
+    z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    xi, eta, ze = (x - 15.5) / h, (y - 13.5) / h, (z - 11.5) / h
+    u = (xi**4 * eta**3 + ze**5).astype(np.float64)
+    lap = (12 * xi**2 * eta**3 + 6 * xi**4 * eta + 20 * ze**3) / h**2
+    nu = 0.4
+    v = np.full(u.shape, nu * 10.0 / 1e-3, np.float32)
+    out = gpu_run(P, v, 10.0, 1e-3, 1, u0=u.astype(np.float32), up0=(2 * u).astype(np.float32))
+    Cf = np.float32(np.float64(v[0, 0, 0]) * 1e-3 / 10.0) ** 2
+    s = (slice(5, -5),) * 3
+    err = np.abs(out[s] - Cf * lap[s]).max()
+    assert err <= 2e-5 * np.abs(u[s]).max() * 8 * Cf
+
+
+def test_time_reversibility_fp32(P):
+    nz, ny, nx = 24, 20, 32
+    rng = np.random.default_rng(1)
+    v = rng.uniform(1500, 4300, (nz, ny, nx)).astype(np.float32)
+    u0, up0 = ri.random_fields(v.shape, seed=77)
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32) as sim:
+        sim.set_velocity(v)
+        sim.set_fields(u0, up0)
+        sim.step(20)
+        uN, uNm1 = sim.read_fields()
+        sim.set_fields(uNm1, uN)
+        sim.step(20)
+        back, back_prev = sim.read_fields()
+    assert np.abs(back - up0).max() <= 1e-4
+    assert np.abs(back_prev - u0).max() <= 1e-4
+
+
+# ----------------------------------------------------------------------------- edges
+@pytest.mark.parametrize("shape", [(1, 1, 4), (1, 9, 8), (11, 1, 12), (3, 5, 7), (2, 3, 1), (13, 17, 20)])
+def test_degenerate_and_tiny_grids(P, shape):
+    v = np.full(shape, 3000.0, np.float32)
+    u0, up0 = ri.random_fields(shape, seed=sum(shape))
+    src = [(0, 0, 0, np.ones(4, np.float32))]
+    ref = oracle.run(v, 10.0, 1e-3, C32, 4, u0=u0, up0=up0, sources=src)
+    got = gpu_run(P, v, 10.0, 1e-3, 4, u0=u0, up0=up0, sources=src)
+    assert relerr(got, ref) <= TOL_1 * 10
+
+
+def test_zero_steps_and_reset(P):
+    v = np.full((8, 8, 8), 3000.0, np.float32)
+    u0, up0 = ri.random_fields(v.shape, seed=2)
+    with P.Simulation(8, 8, 8, 10.0, 1e-3, C32) as sim:
+        sim.set_velocity(v)
+        sim.set_fields(u0, up0)
+        sim.step(0)
+        assert np.array_equal(sim.read_field(), u0)
+        sim.step(3)
+        sim.reset()
+        assert sim.steps_taken == 0 and not np.any(sim.read_field())
+
+
+def test_max_sources_same_point(P):
+    v = np.full((10, 10, 12), 2000.0, np.float32)
+    w = np.linspace(-1, 1, 5).astype(np.float32)
+    src = [(4, 5, 6, w * (k + 1) / 7) for k in range(P.RTM_MAX_SOURCES)]
+    ref = oracle.run(v, 10.0, 1e-3, C32, 5, sources=src)
+    got = gpu_run(P, v, 10.0, 1e-3, 5, sources=src)
+    assert relerr(got, ref) <= 1e-6
+    with P.Simulation(12, 10, 10, 10.0, 1e-3, C32) as sim:
+        for s in src:
+            sim.inject_source(*s)
+        with pytest.raises(P.RtmError):
+            sim.inject_source(1, 1, 1, w)
+
+
+def test_errors_are_reported(P):
+    with P.Simulation(8, 8, 8, 10.0, 1e-3, C32) as sim:
+        with pytest.raises(P.RtmError) as e:
+            sim.step(1)
+        assert e.value.code == P.RTM_ESTATE
+        vlim = ri.NU_CRIT * 10.0 / 1e-3
+        with pytest.raises(P.RtmError) as e:
+            sim.set_velocity(np.full((8, 8, 8), vlim * 1.001, np.float32))
+        assert e.value.code == P.RTM_ECFL and "CFL" in str(e.value)
+        sim.set_velocity(np.full((8, 8, 8), vlim * 0.999, np.float32))
+        bad = np.full((8, 8, 8), 2000.0, np.float32)
+        bad[3, 3, 3] = np.nan
+        with pytest.raises(P.RtmError) as e:
+            sim.set_velocity(bad)
+        assert e.value.code == P.RTM_EINVAL
+        with pytest.raises(P.RtmError) as e:
+            sim.step(1)  # failed set_velocity leaves no velocity installed
+        assert e.value.code == P.RTM_ESTATE
+        with pytest.raises(P.RtmError):
+            sim.inject_source(8, 0, 0, np.ones(2, np.float32))
+        with pytest.raises(P.RtmError):
+            sim.set_tile(P.rtm_num_tiles())
+    with P.Simulation(6, 8, 8, 10.0, 1e-3, C32) as sim:  # nx % 4 != 0 -> naive only
+        assert sim.tile == 0
+        with pytest.raises(P.RtmError):
+            sim.set_tile(1)
+
+
+def test_cfl_growth_at_1_02_nu_crit_is_rejected_and_0_99_is_bounded(P):
+    shape = (32, 32, 32)
+    vlim = ri.NU_CRIT * 10.0 / 1e-3
+    with P.Simulation(32, 32, 32, 10.0, 1e-3, C32) as sim:
+        with pytest.raises(P.RtmError):
+            sim.set_velocity(np.full(shape, 1.02 * vlim, np.float32))
+        sim.set_velocity(np.full(shape, 0.99 * vlim, np.float32))
+        u0, up0 = ri.random_fields(shape, seed=8)
+        sim.set_fields(u0, up0)
+        sim.step(200)
+        assert np.abs(sim.read_field()).max() < 20
+
+
+# ----------------------------------------------------------------------------- torch plumbing
+def test_device_pointer_variants_and_user_stream(P):
+    import torch
+    cfg = ri.make_config(2, shape=(40, 48, 64), steps=30)
+    v = cfg.velocity()
+    src = cfg.sources()
+    ref = gpu_run(P, v, cfg.dx, cfg.dt, 30, sources=src)
+    dv = torch.from_numpy(v).cuda()
+    dout = torch.empty_like(dv)
+    s = torch.cuda.Stream()
+    with P.Simulation(64, 48, 40, cfg.dx, cfg.dt, C32) as sim:
+        for x in src:
+            sim.inject_source(*x)
+        P.rtm_set_stream(sim.h, s.cuda_stream)
+        with torch.cuda.stream(s):
+            P.rtm_set_velocity_device(sim.h, dv.data_ptr())
+            P.rtm_reset(sim.h)
+            P.rtm_step(sim.h, 30)
+            P.rtm_read_field_device(sim.h, dout.data_ptr())
+        s.synchronize()
+        assert np.array_equal(dout.cpu().numpy(), ref)
+        P.rtm_set_profiling(sim.h, 1)
+        P.rtm_step(sim.h, 5)
+        n, ms = P.rtm_kernel_stats(sim.h)
+        assert n == 5 and ms > 0
+        P.rtm_set_stream(sim.h, 0)
