@@ -86,8 +86,11 @@ struct Slab {
     cudaStream_t s_own = nullptr, s_comm = nullptr, s_user = nullptr;
     bool has_user = false;
     cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
-    CUtensorMap tm[2];
+    CUtensorMap tm_u[2];   // u with the halo box, one per time-level buffer
+    CUtensorMap tm_in[2];  // TX x TY box over each buffer (u_prev read of k_stream)
+    CUtensorMap tm_c;      // TX x TY box over C
     int tm_variant = -1;
+    int occupancy = 0;     // resident CTAs per SM of tm_variant
     cudaGraphExec_t graph = nullptr;
     cudaGraph_t graph_def = nullptr;
     int graph_variant = -1;
@@ -273,33 +276,43 @@ int finish_ctx(rtm_ctx* c) {
 int resolve_tile(const rtm_ctx* c) {
     if (c->nx % 4 != 0) return 0;  // 128-bit rows / TMA strides need nx % 4 == 0
     if (c->tile >= 0) return c->tile;
-    return 1;  // tma64x16k10 (tile sweep)
+    return 8;  // stream64x32k10d0: best of the C3/C4 sweep (profiles/sweep_*_r01.log)
+}
+
+int encode_3d(CUtensorMap* tm, void* base, int nx, int ny, int nplanes, int bx, int by) {
+    auto enc = encode_fn();
+    if (!enc) return fail(RTM_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nplanes};
+    cuuint64_t strides[2] = {(cuuint64_t)nx * 4, (cuuint64_t)nx * ny * 4};
+    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return fail(RTM_ECUDA, "cuTensorMapEncodeTiled(box %dx%d) failed (%d)", bx, by, (int)r);
+    return RTM_OK;
 }
 
 int ensure_tmaps(rtm_ctx* c, Slab& s, int var) {
     if (var == 0 || s.tm_variant == var) return RTM_OK;
-    auto enc = encode_fn();
-    if (!enc) return fail(RTM_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
     const TileVariant& tv = variant(var);
-    cuuint64_t dims[3] = {(cuuint64_t)c->nx, (cuuint64_t)c->ny, (cuuint64_t)(s.nzl + 10)};
-    cuuint64_t strides[2] = {(cuuint64_t)c->nx * 4, (cuuint64_t)c->nx * c->ny * 4};
-    cuuint32_t box[3] = {(cuuint32_t)(tv.TX + 16), (cuuint32_t)(tv.TY + 10), 1};
-    cuuint32_t es[3] = {1, 1, 1};
     for (int b = 0; b < 2; ++b) {
-        CUresult r = enc(&s.tm[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, s.buf[b], dims, strides, box,
-                         es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return fail(RTM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+        RET(encode_3d(&s.tm_u[b], s.buf[b], c->nx, c->ny, s.nzl + 10, tv.TX + 16, tv.TY + 10));
+        RET(encode_3d(&s.tm_in[b], s.buf[b], c->nx, c->ny, s.nzl + 10, tv.TX, tv.TY));
     }
+    RET(encode_3d(&s.tm_c, s.C, c->nx, c->ny, s.nzl, tv.TX, tv.TY));
+    int tpb = 0;
+    s.occupancy = variant_occupancy(var, &tpb);
+    if (s.occupancy < 1)
+        return fail(RTM_ECUDA, "variant %s cannot be resident on this device", tv.name);
     s.tm_variant = var;
     return RTM_OK;
 }
 
 // z-chunks for a range of len planes: minimise (wave quantisation) x (chunk-halo re-read).
-int choose_chunks(const rtm_ctx* c, int var, int ntiles, int len) {
+int choose_chunks(const rtm_ctx* c, int occ, int ntiles, int len) {
     if (c->zchunk > 0) return std::max(1, (len + c->zchunk - 1) / c->zchunk);
-    int tpb = 0;
-    int occ = tiled_occupancy(var, &tpb);
     if (occ < 1) occ = 1;
     const double S = (double)c->num_sms * occ;
     int best = 1;
@@ -366,9 +379,10 @@ int launch_stencil(rtm_ctx* c, Slab& s, int parity, int b0, int l0, int b1, int 
         p.tiles_x = (c->nx + tv.TX - 1) / tv.TX;
         p.tiles_y = (c->ny + tv.TY - 1) / tv.TY;
         const int nt = p.tiles_x * p.tiles_y;
-        p.r_chunks[0] = choose_chunks(c, var, nt, l0);
-        p.r_chunks[1] = l1 > 0 ? choose_chunks(c, var, nt, l1) : 0;
-        CK(launch_tiled(var, s.tm[parity], p, st));
+        p.r_chunks[0] = choose_chunks(c, s.occupancy, nt, l0);
+        p.r_chunks[1] = l1 > 0 ? choose_chunks(c, s.occupancy, nt, l1) : 0;
+        CK(launch_variant(var, &s.tm_u[parity], &s.tm_in[parity ^ 1], &s.tm_c, p,
+                          c->num_sms * s.occupancy, st));
     }
     if (c->profiling) {
         CK(cudaEventRecord(e1, st));

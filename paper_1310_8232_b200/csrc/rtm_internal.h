@@ -39,19 +39,23 @@ struct StencilParams {
 
 struct TileVariant {
     const char* name;
-    int TX, TY, K, MINB;       // tile (x, y), TMA ring depth (planes), min blocks per SM
+    int kind;                  // 0 naive, 1 k_tiled (CTA per unit), 2 k_stream (persistent, producer warp)
+    int TX, TY, K, D, MINB;    // tile (x, y), u ring depth, u_prev/C ring depth (0: LDG), min CTAs/SM
 };
 
-// Variant table: index 0 is the naive kernel, 1.. the TMA-tiled kernels.
+// Variant table: index 0 is the naive kernel.
 int num_variants();
 const TileVariant& variant(int id);
 
-// Dynamic shared memory of a tiled variant (bytes).
-size_t tiled_smem_bytes(int id);
-// Max resident blocks per SM of a tiled variant (after opting in to its smem), or <0 on error.
-int tiled_occupancy(int id, int* threads_per_block);
+size_t variant_smem_bytes(int id);
+// Max resident blocks per SM (after opting in to the variant's smem), or < 0 on error.
+int variant_occupancy(int id, int* threads_per_block);
 
-cudaError_t launch_tiled(int id, const CUtensorMap& tm, const StencilParams& p, cudaStream_t s);
+// tm_u: u^n with the (TX+16) x (TY+10) halo box; tm_up: u^{n-1} and tm_c: C with TX x TY
+// boxes (k_stream with D > 0).  max_ctas bounds the persistent grid.
+cudaError_t launch_variant(int id, const CUtensorMap* tm_u, const CUtensorMap* tm_up,
+                           const CUtensorMap* tm_c, const StencilParams& p, int max_ctas,
+                           cudaStream_t s);
 cudaError_t launch_naive(const StencilParams& p, cudaStream_t s);
 
 // a1: C = fp32((double(v)*dt/dx)^2), stats[0] = max(v) bits (v > 0), stats[1] = count of

@@ -349,64 +349,306 @@ __global__ void __launch_bounds__(256) k_velocity(const float* v, float* C, long
 }
 
 // ------------------------------------------------------------------------------------
-// Variant table.  id 0 = naive.
-#define RTM_TILED_VARIANTS(X)            \
-    X(1, "tma64x16k10", 64, 16, 10, 2)   \
-    X(2, "tma32x16k10", 32, 16, 10, 3)   \
-    X(3, "tma64x8k10", 64, 8, 10, 3)     \
-    X(4, "tma128x8k10", 128, 8, 10, 2)   \
-    X(5, "tma32x32k10", 32, 32, 10, 2)   \
-    X(6, "tma64x16k12", 64, 16, 12, 2)   \
-    X(7, "tma128x16k10", 128, 16, 10, 1) \
-    X(8, "tma64x32k10", 64, 32, 10, 1)   \
-    X(9, "tma32x8k10", 32, 8, 10, 4)
+// k_stream: warp-specialised persistent version of k_tiled.  One producer warp streams,
+// unit after unit, the halo'd u planes (TMA, K-slot ring) and — when D > 0 — the u_prev and
+// C tiles (TMA, D-slot ring) into shared memory; NW consumer warps compute.  Slots are
+// handed over with full/empty mbarriers only (no CTA-wide barrier in the loop), so each
+// consumer warp runs ahead as far as the data allows and the producer prefetches across
+// unit boundaries.  Work units are (z-chunk, tile) pairs, chunk-major, dealt round-robin
+// to the persistent CTAs (unit = blockIdx.x + k * gridDim.x) so co-running CTAs are xy
+// neighbours at similar z.
+template <int TX, int TY, int K, int D>
+struct StreamShape {
+    static constexpr int NW = TX * TY / 128;      // consumer warps (4 points per thread)
+    static constexpr int NT = NW * 32 + 32;       // + 1 producer warp
+    static constexpr int TXV = TX / 4;
+    static constexpr int RS = TX + 16;
+    static constexpr int ROWS = TY + 10;
+    static constexpr int USLOT = (RS * ROWS + 31) / 32 * 32;
+    static constexpr uint32_t UBYTES = RS * ROWS * 4;
+    static constexpr int CSLOT = 2 * TX * TY;     // u_prev tile then C tile
+    static constexpr uint32_t CBYTES = CSLOT * 4;
+    static constexpr size_t BAR_OFF = (size_t(K) * USLOT + size_t(D) * CSLOT) * 4;
+    static constexpr size_t SMEM = BAR_OFF + size_t(2 * K + 2 * D) * 8;
+    static_assert((TX * TY) % 128 == 0, "whole consumer warps");
+    static_assert(K >= 7, "6 live planes + 1 in flight");
+    static_assert(TX % 4 == 0 && RS <= 256 && ROWS <= 256 && TX <= 256 && TY <= 256, "TMA box");
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
+
+struct UnitGeom {
+    int x0, y0, zs, ze;
+};
+__device__ __forceinline__ UnitGeom unit_geom(const StencilParams& p, int unit, int TX, int TY) {
+    const int ntiles = p.tiles_x * p.tiles_y;
+    int chunk = unit / ntiles;
+    const int tile = unit - chunk * ntiles;
+    int r = 0;
+    if (chunk >= p.r_chunks[0]) {
+        r = 1;
+        chunk -= p.r_chunks[0];
+    }
+    UnitGeom g;
+    g.zs = p.r_begin[r] + static_cast<int>((long long)chunk * p.r_len[r] / p.r_chunks[r]);
+    g.ze = p.r_begin[r] + static_cast<int>((long long)(chunk + 1) * p.r_len[r] / p.r_chunks[r]);
+    const int tyi = tile / p.tiles_x;
+    g.x0 = (tile - tyi * p.tiles_x) * TX;
+    g.y0 = tyi * TY;
+    return g;
+}
+
+template <int TX, int TY, int K, int D, int MINB>
+__global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
+    k_stream(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_up,
+             const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ StencilParams p) {
+    using S = StreamShape<TX, TY, K, D>;
+    extern __shared__ __align__(128) float smem[];
+    float* uring = smem;
+    float* cring = smem + K * S::USLOT;
+    uint64_t* full_u = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + S::BAR_OFF);
+    uint64_t* empty_u = full_u + K;
+    uint64_t* full_c = empty_u + K;
+    uint64_t* empty_c = full_c + D;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) {
+        for (int k = 0; k < K; ++k) {
+            mbar_init(&full_u[k], 1);
+            mbar_init(&empty_u[k], S::NW);
+        }
+        for (int k = 0; k < D; ++k) {
+            mbar_init(&full_c[k], 1);
+            mbar_init(&empty_c[k], S::NW);
+        }
+        fence_mbar_init();
+    }
+    if (p.write_next && blockIdx.x == 0 && tid == 0)
+        p.d_step[p.parity ^ 1] = p.d_step[p.parity] + 1;
+    __syncthreads();
+
+    const int units = p.tiles_x * p.tiles_y * (p.r_chunks[0] + (p.nranges > 1 ? p.r_chunks[1] : 0));
+
+    if (warp == S::NW) {  // ---------------- producer warp
+        if (lane == 0) {
+            uint32_t gu = 0, gc = 0;
+            for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
+                const UnitGeom g = unit_geom(p, unit, TX, TY);
+                const int n = g.ze - g.zs;
+                auto put_u = [&](int j) {
+                    const uint32_t seq = gu + j, slot = seq % K;
+                    if (seq >= K) mbar_wait(&empty_u[slot], ((seq / K) - 1) & 1);
+                    mbar_expect_tx(&full_u[slot], S::UBYTES);
+                    tma_load_3d(uring + slot * S::USLOT, &tm_u, g.x0 - 8, g.y0 - 5, g.zs + j,
+                                &full_u[slot]);
+                };
+                auto put_c = [&](int i) {
+                    const uint32_t seq = gc + i, slot = seq % D;
+                    if (seq >= D) mbar_wait(&empty_c[slot], ((seq / D) - 1) & 1);
+                    mbar_expect_tx(&full_c[slot], S::CBYTES);
+                    float* dst = cring + slot * S::CSLOT;
+                    tma_load_3d(dst, &tm_up, g.x0, g.y0, g.zs + i + 5, &full_c[slot]);
+                    tma_load_3d(dst + TX * TY, &tm_c, g.x0, g.y0, g.zs + i, &full_c[slot]);
+                };
+                for (int j = 0; j < 10; ++j) put_u(j);
+                for (int i = 0; i < n; ++i) {
+                    if constexpr (D > 0) put_c(i);
+                    put_u(i + 10);
+                }
+                gu += n + 10;
+                gc += n;
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumer warps
+    const int tx = tid % S::TXV, ty = tid / S::TXV;
+    const int own = (5 + ty) * S::RS + 8 + 4 * tx;
+    const int cown = ty * TX + 4 * tx;
+    const float c[6] = {p.coef[0], p.coef[1], p.coef[2], p.coef[3], p.coef[4], p.coef[5]};
+    uint32_t gu = 0, gc = 0;
+    auto release_u = [&](uint32_t seq) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_u[seq % K]);
+    };
+    for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
+        const UnitGeom g = unit_geom(p, unit, TX, TY);
+        const int n = g.ze - g.zs;
+        const int x = g.x0 + 4 * tx, y = g.y0 + ty;
+        const bool active = (x < p.nx) && (y < p.ny);
+        uint64_t smask = 0;
+        if (active) {
+            for (int s = 0; s < p.nsrc; ++s) {
+                const DevSource& src = p.src[s];
+                if (src.y == y && src.x >= x && src.x < x + 4 && src.z >= g.zs && src.z < g.ze)
+                    smask |= (1ull << s);
+            }
+        }
+        const long long col = (long long)y * p.nx + x;
+        float* outp = p.next + (long long)(g.zs + 5) * p.plane + col;  // also u_prev (D == 0)
+        const float* cp = p.C + (long long)g.zs * p.plane + col;
+
+        float4 q[11];
+#pragma unroll
+        for (int j = 0; j < 10; ++j) {
+            const uint32_t seq = gu + j;
+            mbar_wait(&full_u[seq % K], (seq / K) & 1);
+            q[j] = *reinterpret_cast<const float4*>(uring + (seq % K) * S::USLOT + own);
+            if (j < 5) release_u(seq);
+        }
+        float4 upv = make_float4(0.f, 0.f, 0.f, 0.f), cv = upv;
+        if constexpr (D == 0) {
+            if (active) {
+                upv = ld_stream4(outp);
+                cv = ld_stream4(cp);
+            }
+        }
+#pragma unroll 1
+        for (int i = 0; i < n; ++i) {
+            float4 upn = upv, cn = cv;
+            if constexpr (D == 0) {
+                if (active && i + 1 < n) {
+                    upn = ld_stream4(outp + p.plane);
+                    cn = ld_stream4(cp + p.plane);
+                    if (i + 4 < n) {
+                        prefetch_l2(outp + 4 * p.plane);
+                        prefetch_l2(cp + 4 * p.plane);
+                    }
+                }
+            }
+            const uint32_t sn = gu + i + 10, sc = gu + i + 5;
+            mbar_wait(&full_u[sn % K], (sn / K) & 1);
+            q[10] = *reinterpret_cast<const float4*>(uring + (sn % K) * S::USLOT + own);
+            if constexpr (D > 0) {
+                const uint32_t cs = gc + i;
+                mbar_wait(&full_c[cs % D], (cs / D) & 1);
+                const float* cb = cring + (cs % D) * S::CSLOT + cown;
+                upv = *reinterpret_cast<const float4*>(cb);
+                cv = *reinterpret_cast<const float4*>(cb + TX * TY);
+            }
+            const float* row = uring + (sc % K) * S::USLOT + own;
+            float xs[14];
+            {
+                const float4 l = *reinterpret_cast<const float4*>(row - 4);
+                const float4 rr = *reinterpret_cast<const float4*>(row + 4);
+                xs[0] = row[-5];
+                xs[1] = l.x; xs[2] = l.y; xs[3] = l.z; xs[4] = l.w;
+                xs[5] = q[5].x; xs[6] = q[5].y; xs[7] = q[5].z; xs[8] = q[5].w;
+                xs[9] = rr.x; xs[10] = rr.y; xs[11] = rr.z; xs[12] = rr.w;
+                xs[13] = row[8];
+            }
+            float4 yv[11];
+#pragma unroll
+            for (int m = 1; m <= 5; ++m) {
+                yv[5 - m] = *reinterpret_cast<const float4*>(row - m * S::RS);
+                yv[5 + m] = *reinterpret_cast<const float4*>(row + m * S::RS);
+            }
+            yv[5] = q[5];
+            float out[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                float zl[11], yl[11], xl[11];
+#pragma unroll
+                for (int o = 0; o < 11; ++o) {
+                    zl[o] = comp(q[o], k);
+                    yl[o] = comp(yv[o], k);
+                    xl[o] = xs[k + o];
+                }
+                out[k] = rtm_point(zl, yl, xl, comp(upv, k), comp(cv, k), c);
+            }
+            release_u(sc);
+            if constexpr (D > 0) {
+                if (lane == 0) mbar_arrive(&empty_c[(gc + i) % D]);  // after the same __syncwarp
+            }
+            if (smask) add_sources(p, smask, x, g.zs + i, out);
+            if (active) st_stream4(outp, make_float4(out[0], out[1], out[2], out[3]));
+#pragma unroll
+            for (int o = 0; o < 10; ++o) q[o] = q[o + 1];
+            upv = upn;
+            cv = cn;
+            outp += p.plane;
+            cp += p.plane;
+        }
+#pragma unroll 1
+        for (int j = n + 5; j < n + 10; ++j) release_u(gu + j);  // planes used only by the queue
+        gu += n + 10;
+        gc += n;
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// Variant table.  id 0 = naive; kind 1 = k_tiled; kind 2 = k_stream.
+#define RTM_VARIANTS(X)                               \
+    X(1, "stream64x16k8d4", 2, 64, 16, 8, 4, 2)       \
+    X(2, "stream64x16k9d0", 2, 64, 16, 9, 0, 2)       \
+    X(3, "stream64x32k8d3", 2, 64, 32, 8, 3, 1)       \
+    X(4, "stream128x16k8d3", 2, 128, 16, 8, 3, 1)     \
+    X(5, "stream32x32k8d4", 2, 32, 32, 8, 4, 2)       \
+    X(6, "stream64x8k8d4", 2, 64, 8, 8, 4, 3)         \
+    X(7, "stream128x8k8d4", 2, 128, 8, 8, 4, 2)       \
+    X(8, "stream64x32k10d0", 2, 64, 32, 10, 0, 1)     \
+    X(9, "tma64x16k10", 1, 64, 16, 10, 0, 2)          \
+    X(10, "tma32x16k10", 1, 32, 16, 10, 0, 3)         \
+    X(11, "tma64x8k10", 1, 64, 8, 10, 0, 3)           \
+    X(12, "tma128x8k10", 1, 128, 8, 10, 0, 2)         \
+    X(13, "tma32x32k10", 1, 32, 32, 10, 0, 2)
 
 static const TileVariant kVariants[] = {
-    {"naive", 0, 0, 0, 0},
-#define X(id, name, tx, ty, k, mb) {name, tx, ty, k, mb},
-    RTM_TILED_VARIANTS(X)
+    {"naive", 0, 0, 0, 0, 0, 0},
+#define X(id, name, kind, tx, ty, k, d, mb) {name, kind, tx, ty, k, d, mb},
+    RTM_VARIANTS(X)
 #undef X
 };
 
 int num_variants() { return static_cast<int>(sizeof(kVariants) / sizeof(kVariants[0])); }
 const TileVariant& variant(int id) { return kVariants[id]; }
 
-size_t tiled_smem_bytes(int id) {
-    switch (id) {
-#define X(vid, name, tx, ty, k, mb) \
-    case vid:                       \
-        return TiledShape<tx, ty, k>::SMEM;
-        RTM_TILED_VARIANTS(X)
-#undef X
-        default:
-            return 0;
-    }
-}
-
-template <int TX, int TY, int K, int MINB>
+template <int KIND, int TX, int TY, int K, int D, int MINB>
 static cudaError_t prepare(const void** fn, int* threads, size_t* smem) {
-    using S = TiledShape<TX, TY, K>;
-    *fn = reinterpret_cast<const void*>(&k_tiled<TX, TY, K, MINB>);
-    *threads = S::NT;
-    *smem = S::SMEM;
-    return cudaFuncSetAttribute(&k_tiled<TX, TY, K, MINB>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(S::SMEM));
+    if constexpr (KIND == 1) {
+        using S = TiledShape<TX, TY, K>;
+        *fn = reinterpret_cast<const void*>(&k_tiled<TX, TY, K, MINB>);
+        *threads = S::NT;
+        *smem = S::SMEM;
+    } else {
+        using S = StreamShape<TX, TY, K, D>;
+        *fn = reinterpret_cast<const void*>(&k_stream<TX, TY, K, D, MINB>);
+        *threads = S::NT;
+        *smem = S::SMEM;
+    }
+    return cudaFuncSetAttribute(*fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(*smem));
 }
 
 static cudaError_t variant_fn(int id, const void** fn, int* threads, size_t* smem) {
     switch (id) {
-#define X(vid, name, tx, ty, k, mb) \
-    case vid:                       \
-        return prepare<tx, ty, k, mb>(fn, threads, smem);
-        RTM_TILED_VARIANTS(X)
+#define X(vid, name, kind, tx, ty, k, d, mb) \
+    case vid:                                \
+        return prepare<kind, tx, ty, k, d, mb>(fn, threads, smem);
+        RTM_VARIANTS(X)
 #undef X
         default:
             return cudaErrorInvalidValue;
     }
 }
 
-int tiled_occupancy(int id, int* threads_per_block) {
+size_t variant_smem_bytes(int id) {
+    const void* fn;
+    int threads;
+    size_t smem = 0;
+    if (variant_fn(id, &fn, &threads, &smem) != cudaSuccess) return 0;
+    return smem;
+}
+
+int variant_occupancy(int id, int* threads_per_block) {
     const void* fn;
     int threads;
     size_t smem;
@@ -418,7 +660,9 @@ int tiled_occupancy(int id, int* threads_per_block) {
     return nb;
 }
 
-cudaError_t launch_tiled(int id, const CUtensorMap& tm, const StencilParams& p, cudaStream_t s) {
+cudaError_t launch_variant(int id, const CUtensorMap* tm_u, const CUtensorMap* tm_up,
+                           const CUtensorMap* tm_c, const StencilParams& p, int max_ctas,
+                           cudaStream_t s) {
     const void* fn;
     int threads;
     size_t smem;
@@ -427,8 +671,14 @@ cudaError_t launch_tiled(int id, const CUtensorMap& tm, const StencilParams& p, 
     const long long units = (long long)p.tiles_x * p.tiles_y *
                             (p.r_chunks[0] + (p.nranges > 1 ? p.r_chunks[1] : 0));
     if (units <= 0) return cudaSuccess;
-    void* args[] = {const_cast<CUtensorMap*>(&tm), const_cast<StencilParams*>(&p)};
-    return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(units)), dim3(threads), args, smem, s);
+    if (variant(id).kind == 1) {
+        void* args[] = {const_cast<CUtensorMap*>(tm_u), const_cast<StencilParams*>(&p)};
+        return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(units)), dim3(threads), args, smem, s);
+    }
+    const long long grid = units < max_ctas ? units : max_ctas;
+    void* args[] = {const_cast<CUtensorMap*>(tm_u), const_cast<CUtensorMap*>(tm_up),
+                    const_cast<CUtensorMap*>(tm_c), const_cast<StencilParams*>(&p)};
+    return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(threads), args, smem, s);
 }
 
 cudaError_t launch_naive(const StencilParams& p, cudaStream_t s) {

@@ -1,0 +1,59 @@
+"""Tile-variant sweep on a config's real grid (the GPU analogue of the paper's blocksize
+selection phase): every variant runs nI time steps from the config's
+state, timed with CUDA events; prints ms/step, Gpt/s and effective GB/s per variant."""
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import numpy as np  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--ni", type=int, default=20)
+    ap.add_argument("--tiles", default="")
+    ap.add_argument("--zchunk", default="0")
+    args = ap.parse_args()
+    import torch
+    import paper_1310_8232_b200 as P
+    import rtm_inputs as ri
+    cfg = ri.make_config(args.config)
+    v = cfg.velocity()
+    h = P.rtm_create(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32)
+    P.rtm_set_velocity(h, v)
+    for s in cfg.sources(v):
+        P.rtm_inject_source(h, *s)
+    st = torch.cuda.Stream()
+    P.rtm_set_stream(h, st.cuda_stream)
+    tiles = [int(t) for t in args.tiles.split(",")] if args.tiles else list(range(P.rtm_num_tiles()))
+    res = []
+    for t in tiles:
+        for zc in [int(z) for z in args.zchunk.split(",")]:
+            P.rtm_set_tile(h, t)
+            P.rtm_set_zchunk(h, zc)
+            P.rtm_reset(h)
+            P.rtm_step(h, 4)  # warm-up (graphs, tensor maps)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            P.rtm_step(h, args.ni)
+            e1.record(st)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / args.ni
+            gpts = cfg.points / ms / 1e6
+            r = {"tile": t, "name": P.rtm_tile_name(t), "zchunk": zc, "ms_per_step": round(ms, 4),
+                 "gpts": round(gpts, 2), "eff_gbs": round(16 * gpts, 1)}
+            res.append(r)
+            print(json.dumps(r), flush=True)
+    best = min(res, key=lambda r: r["ms_per_step"])
+    print("BEST", json.dumps(best))
+    P.rtm_destroy(h)
+
+
+if __name__ == "__main__":
+    main()
