@@ -183,7 +183,10 @@ def cpu_baseline(cfg, v_full):
     t = time.perf_counter()
     oracle.run(v, cfg.dx, cfg.dt, ri.COEFFS_F32, 1, nthreads=cores)
     t1 = time.perf_counter() - t
-    n = int(max(1, min(50, 10.0 / max(t1, 1e-3))))
+    t = time.perf_counter()
+    oracle.run(v, cfg.dx, cfg.dt, ri.COEFFS_F32, 3, nthreads=cores)
+    per_step = max((time.perf_counter() - t - t1) / 2, 1e-3)  # marginal cost of a step
+    n = int(max(1, min(200, 12.0 / per_step)))
     t = time.perf_counter()
     oracle.run(v, cfg.dx, cfg.dt, ri.COEFFS_F32, n, nthreads=cores)
     dt = time.perf_counter() - t

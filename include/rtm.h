@@ -112,7 +112,20 @@ int rtm_num_tiles(void);
 /* z-chunk length (planes) of a tiled work unit; 0 = automatic (minimises wave quantisation
  * times chunk-halo re-reads). */
 int rtm_set_zchunk(rtm_ctx* ctx, int planes);
-const char* rtm_tile_name(int tile_id);  /* e.g. "tma64x16k10"; NULL for unknown ids */
+const char* rtm_tile_name(int tile_id);  /* e.g. "stream64x32k10d0"; NULL for unknown ids */
+
+/* Tuning options (results are bitwise independent of all of them):
+ *   RTM_OPT_ZCHUNK     z-chunk length in planes, 0 = automatic (same as rtm_set_zchunk)
+ *   RTM_OPT_CACHE_MODE L2 policy bits of the stream kernels: bits 0-1 L2 prefetch of u_prev/C
+ *                      (0 none, 1 evict_last, 2 evict_normal), bit 2 u TMA loads with an
+ *                      evict_last policy, bit 3 plain (not evict-first) u_prev/C/u_next
+ *                      accesses, bits 4-7 prefetch distance in planes, bits 8-9 L2 promotion
+ *                      of the halo'd u TMA box (0 = 256B, 1 = 128B, 2 = 64B, 3 = none)
+ *   RTM_OPT_GRAPHS     1 (default) = capture runs of 16 steps in CUDA graphs, 0 = direct launches
+ * Unknown key or out-of-range value -> RTM_EINVAL.  rtm_get_option returns -1 for unknown keys. */
+enum { RTM_OPT_ZCHUNK = 1, RTM_OPT_CACHE_MODE = 2, RTM_OPT_GRAPHS = 3 };
+int rtm_set_option(rtm_ctx* ctx, int key, long long value);
+long long rtm_get_option(rtm_ctx* ctx, int key);
 
 /* Run on the caller's CUDA stream (a cudaStream_t, e.g. torch.cuda.current_stream()); NULL
  * restores the library's own stream.  Single-GPU or distributed (one slab per process)

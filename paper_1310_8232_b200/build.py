@@ -1,6 +1,6 @@
 """Build the in-tree C-ABI shared library ``librtm_b200.so`` for sm_100a with nvcc.
 
-    python -m paper_1310_8232_b200.build [--verbose]
+    python paper_1310_8232_b200/build.py [--verbose]   (standalone: does not import the package)
 
 Kernels (csrc/rtm_kernels.cu) and the host library (csrc/rtm_host.cpp) are compiled with
 ``-gencode arch=compute_100a,code=sm_100a -lineinfo`` and linked against the NCCL 2.28

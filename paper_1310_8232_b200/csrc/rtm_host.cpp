@@ -113,6 +113,8 @@ struct rtm_ctx {
     bool vel_set = false;
     int tile = -1;
     int zchunk = 0;  // 0 = auto
+    int cache_mode = 0x41;  // L2 prefetch of u_prev/C 4 planes ahead, evict_last (tuned)
+    bool graphs = true;
     std::vector<HostSource> sources;
     bool profiling = false;
     std::vector<cudaEvent_t> prof_ev;
@@ -276,10 +278,11 @@ int finish_ctx(rtm_ctx* c) {
 int resolve_tile(const rtm_ctx* c) {
     if (c->nx % 4 != 0) return 0;  // 128-bit rows / TMA strides need nx % 4 == 0
     if (c->tile >= 0) return c->tile;
-    return 8;  // stream64x32k10d0: best of the C3/C4 sweep (profiles/sweep_*_r01.log)
+    return 1;  // stream64x16k8d4: best/near-best on C3 and C4 (profiles/sweep_*_r01*.log)
 }
 
-int encode_3d(CUtensorMap* tm, void* base, int nx, int ny, int nplanes, int bx, int by) {
+int encode_3d(CUtensorMap* tm, void* base, int nx, int ny, int nplanes, int bx, int by,
+              int promo = 3) {
     auto enc = encode_fn();
     if (!enc) return fail(RTM_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
     cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nplanes};
@@ -288,17 +291,24 @@ int encode_3d(CUtensorMap* tm, void* base, int nx, int ny, int nplanes, int bx, 
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                     : promo == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                     : promo == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                  : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
         return fail(RTM_ECUDA, "cuTensorMapEncodeTiled(box %dx%d) failed (%d)", bx, by, (int)r);
     return RTM_OK;
 }
 
 int ensure_tmaps(rtm_ctx* c, Slab& s, int var) {
-    if (var == 0 || s.tm_variant == var) return RTM_OK;
+    // promotion of the halo'd u box: cache_mode bits 8-9 hold 3 - promo (0 = 256B default)
+    const int promo = 3 - ((c->cache_mode >> 8) & 3);
+    const int key = var * 4 + promo;
+    if (var == 0 || s.tm_variant == key) return RTM_OK;
     const TileVariant& tv = variant(var);
     for (int b = 0; b < 2; ++b) {
-        RET(encode_3d(&s.tm_u[b], s.buf[b], c->nx, c->ny, s.nzl + 10, tv.TX + 16, tv.TY + 10));
+        RET(encode_3d(&s.tm_u[b], s.buf[b], c->nx, c->ny, s.nzl + 10, tv.TX + 16, tv.TY + 10, promo));
         RET(encode_3d(&s.tm_in[b], s.buf[b], c->nx, c->ny, s.nzl + 10, tv.TX, tv.TY));
     }
     RET(encode_3d(&s.tm_c, s.C, c->nx, c->ny, s.nzl, tv.TX, tv.TY));
@@ -306,7 +316,7 @@ int ensure_tmaps(rtm_ctx* c, Slab& s, int var) {
     s.occupancy = variant_occupancy(var, &tpb);
     if (s.occupancy < 1)
         return fail(RTM_ECUDA, "variant %s cannot be resident on this device", tv.name);
-    s.tm_variant = var;
+    s.tm_variant = key;
     return RTM_OK;
 }
 
@@ -345,6 +355,7 @@ void fill_params(const rtm_ctx* c, const Slab& s, int parity, StencilParams& p) 
     p.nsrc = (int)s.srcs.size();
     for (int k = 0; k < p.nsrc; ++k) p.src[k] = s.srcs[k];
     p.samples = s.d_samples;
+    p.cache_mode = c->cache_mode;
 }
 
 // Launch the stencil on planes [b0,b0+l0) (+ [b1,b1+l1) if l1 > 0) of slab s.
@@ -455,7 +466,7 @@ int step_single(rtm_ctx* c, int nsteps) {
     int k = 0;
     while (k < nsteps) {
         const int parity = (int)(c->step & 1);
-        if (!c->profiling && parity == 0 && nsteps - k >= 2 * GRAPH_PAIRS) {
+        if (c->graphs && !c->profiling && parity == 0 && nsteps - k >= 2 * GRAPH_PAIRS) {
             RET(build_graph(c, s));
             CK(cudaGraphLaunch(s.graph, st));
             c->step += 2 * GRAPH_PAIRS;
@@ -970,6 +981,37 @@ int rtm_set_zchunk(rtm_ctx* c, int planes) {
     c->zchunk = planes;
     invalidate_graphs(c);
     return RTM_OK;
+}
+
+int rtm_set_option(rtm_ctx* c, int key, long long value) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    switch (key) {
+        case RTM_OPT_ZCHUNK:
+            if (value < 0 || value > (1 << 30)) return fail(RTM_EINVAL, "zchunk %lld out of range", value);
+            c->zchunk = (int)value;
+            break;
+        case RTM_OPT_CACHE_MODE:
+            if (value < 0 || value > 0x3ff) return fail(RTM_EINVAL, "cache mode %lld out of range", value);
+            c->cache_mode = (int)value;
+            break;
+        case RTM_OPT_GRAPHS:
+            c->graphs = value != 0;
+            break;
+        default:
+            return fail(RTM_EINVAL, "unknown option key %d", key);
+    }
+    invalidate_graphs(c);
+    return RTM_OK;
+}
+
+long long rtm_get_option(rtm_ctx* c, int key) {
+    if (!c) return -1;
+    switch (key) {
+        case RTM_OPT_ZCHUNK: return c->zchunk;
+        case RTM_OPT_CACHE_MODE: return c->cache_mode;
+        case RTM_OPT_GRAPHS: return c->graphs ? 1 : 0;
+        default: return -1;
+    }
 }
 
 int rtm_set_stream(rtm_ctx* c, void* stream) {

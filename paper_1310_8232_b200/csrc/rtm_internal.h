@@ -32,6 +32,7 @@ struct StencilParams {
     int r_begin[2], r_len[2];  // ranges [r_begin, r_begin + r_len)
     int r_chunks[2];           // z-chunks per range (tiled kernel work units)
     int tiles_x, tiles_y;      // tiled kernel: xy tiles
+    int cache_mode;            // k_stream L2 policy knobs (see rtm_kernels.cu)
     int nsrc;
     DevSource src[RTM_MAX_SOURCES];
     const float* samples;

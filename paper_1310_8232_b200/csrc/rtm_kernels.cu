@@ -379,8 +379,36 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
                  : "memory");
 }
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+// cache_mode (StencilParams): bits 0-1 L2 prefetch of u_prev/C (0 none, 1 evict_last,
+// 2 evict_normal); bit 2 u TMA loads with an evict_last L2 policy; bit 3 plain (not
+// evict-first) u_prev/C loads and u_next stores; bits 4-7 prefetch distance in planes.
+__device__ __forceinline__ void prefetch_l2(const void* p, int mode) {
+    if (mode == 1)
+        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+    else if (mode == 2)
+        asm volatile("prefetch.global.L2::evict_normal [%0];" ::"l"(p));
+}
+__device__ __forceinline__ float4 ld_mode4(const float* p, bool plain) {
+    return plain ? __ldcg(reinterpret_cast<const float4*>(p)) : ld_stream4(p);
+}
+__device__ __forceinline__ void st_mode4(float* p, float4 v, bool plain) {
+    if (plain)
+        __stcg(reinterpret_cast<float4*>(p), v);
+    else
+        st_stream4(p, v);
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* tm, int x, int y,
+                                                 int z, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
 }
 
 struct UnitGeom {
@@ -438,6 +466,8 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
 
     if (warp == S::NW) {  // ---------------- producer warp
         if (lane == 0) {
+            const bool hint = (p.cache_mode & 4) != 0;
+            const uint64_t pol = policy_evict_last();
             uint32_t gu = 0, gc = 0;
             for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
                 const UnitGeom g = unit_geom(p, unit, TX, TY);
@@ -446,8 +476,12 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
                     const uint32_t seq = gu + j, slot = seq % K;
                     if (seq >= K) mbar_wait(&empty_u[slot], ((seq / K) - 1) & 1);
                     mbar_expect_tx(&full_u[slot], S::UBYTES);
-                    tma_load_3d(uring + slot * S::USLOT, &tm_u, g.x0 - 8, g.y0 - 5, g.zs + j,
-                                &full_u[slot]);
+                    if (hint)
+                        tma_load_3d_hint(uring + slot * S::USLOT, &tm_u, g.x0 - 8, g.y0 - 5,
+                                         g.zs + j, &full_u[slot], pol);
+                    else
+                        tma_load_3d(uring + slot * S::USLOT, &tm_u, g.x0 - 8, g.y0 - 5, g.zs + j,
+                                    &full_u[slot]);
                 };
                 auto put_c = [&](int i) {
                     const uint32_t seq = gc + i, slot = seq % D;
@@ -474,6 +508,9 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
     const int own = (5 + ty) * S::RS + 8 + 4 * tx;
     const int cown = ty * TX + 4 * tx;
     const float c[6] = {p.coef[0], p.coef[1], p.coef[2], p.coef[3], p.coef[4], p.coef[5]};
+    const int pf_mode = p.cache_mode & 3;
+    const int pf_dist = (p.cache_mode >> 4) & 15;
+    const bool plain = (p.cache_mode & 8) != 0;
     uint32_t gu = 0, gc = 0;
     auto release_u = [&](uint32_t seq) {
         __syncwarp();
@@ -507,8 +544,8 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
         float4 upv = make_float4(0.f, 0.f, 0.f, 0.f), cv = upv;
         if constexpr (D == 0) {
             if (active) {
-                upv = ld_stream4(outp);
-                cv = ld_stream4(cp);
+                upv = ld_mode4(outp, plain);
+                cv = ld_mode4(cp, plain);
             }
         }
 #pragma unroll 1
@@ -516,11 +553,11 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
             float4 upn = upv, cn = cv;
             if constexpr (D == 0) {
                 if (active && i + 1 < n) {
-                    upn = ld_stream4(outp + p.plane);
-                    cn = ld_stream4(cp + p.plane);
-                    if (i + 4 < n) {
-                        prefetch_l2(outp + 4 * p.plane);
-                        prefetch_l2(cp + 4 * p.plane);
+                    upn = ld_mode4(outp + p.plane, plain);
+                    cn = ld_mode4(cp + p.plane, plain);
+                    if (pf_mode && i + pf_dist < n) {
+                        prefetch_l2(outp + pf_dist * p.plane, pf_mode);
+                        prefetch_l2(cp + pf_dist * p.plane, pf_mode);
                     }
                 }
             }
@@ -569,7 +606,7 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
                 if (lane == 0) mbar_arrive(&empty_c[(gc + i) % D]);  // after the same __syncwarp
             }
             if (smask) add_sources(p, smask, x, g.zs + i, out);
-            if (active) st_stream4(outp, make_float4(out[0], out[1], out[2], out[3]));
+            if (active) st_mode4(outp, make_float4(out[0], out[1], out[2], out[3]), plain);
 #pragma unroll
             for (int o = 0; o < 10; ++o) q[o] = q[o + 1];
             upv = upn;

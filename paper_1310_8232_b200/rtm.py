@@ -17,6 +17,7 @@ _LIB_PATH = Path(__file__).resolve().parent / "librtm_b200.so"
 
 RTM_OK, RTM_EINVAL, RTM_ECFL, RTM_ENOMEM, RTM_ECUDA, RTM_ENCCL, RTM_ESTATE = 0, -1, -2, -3, -4, -5, -6
 RTM_MAX_SOURCES = 64
+RTM_OPT_ZCHUNK, RTM_OPT_CACHE_MODE, RTM_OPT_GRAPHS = 1, 2, 3
 _NAMES = {0: "RTM_OK", -1: "RTM_EINVAL", -2: "RTM_ECFL", -3: "RTM_ENOMEM", -4: "RTM_ECUDA",
           -5: "RTM_ENCCL", -6: "RTM_ESTATE"}
 
@@ -28,7 +29,7 @@ class RtmError(RuntimeError):
 
 
 if not _LIB_PATH.exists():
-    raise ImportError(f"{_LIB_PATH} not built; run python -m paper_1310_8232_b200.build "
+    raise ImportError(f"{_LIB_PATH} not built; run python paper_1310_8232_b200/build.py "
                       "(the product has no CPU fallback)")
 lib = ctypes.CDLL(str(_LIB_PATH))
 
@@ -51,6 +52,8 @@ _SIGS = {
     "rtm_get_tile": (_I, [_P]),
     "rtm_num_tiles": (_I, []),
     "rtm_set_zchunk": (_I, [_P, _I]),
+    "rtm_set_option": (_I, [_P, _I, _LL]),
+    "rtm_get_option": (_LL, [_P, _I]),
     "rtm_tile_name": (ctypes.c_char_p, [_I]),
     "rtm_set_stream": (_I, [_P, _P]),
     "rtm_last_elapsed_ms": (_F, [_P]),
@@ -183,6 +186,14 @@ def rtm_tile_name(tile_id) -> str | None:
 
 def rtm_set_zchunk(h, planes):
     return _check(lib.rtm_set_zchunk(h, int(planes)))
+
+
+def rtm_set_option(h, key, value):
+    return _check(lib.rtm_set_option(h, int(key), int(value)))
+
+
+def rtm_get_option(h, key) -> int:
+    return int(lib.rtm_get_option(h, int(key)))
 
 
 def rtm_set_stream(h, stream_handle):

@@ -19,3 +19,13 @@ def oracle_lib():
     import oracle
     oracle.lib()
     return oracle
+
+
+def build_library():
+    """(Re)build librtm_b200.so via the standalone build script (without importing the
+    package, whose import loads the library)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("rtm_build", ROOT / "paper_1310_8232_b200" / "build.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod.build()

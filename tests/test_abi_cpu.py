@@ -15,8 +15,8 @@ ROOT = Path(__file__).resolve().parent.parent
 
 @pytest.fixture(scope="module")
 def P():
-    from paper_1310_8232_b200 import build
-    build.build()
+    from conftest import build_library
+    build_library()
     import paper_1310_8232_b200 as P
     return P
 

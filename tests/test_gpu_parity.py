@@ -22,8 +22,8 @@ def P():
     import torch
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
-    from paper_1310_8232_b200 import build
-    build.build()
+    from conftest import build_library
+    build_library()
     import paper_1310_8232_b200 as P
     return P
 

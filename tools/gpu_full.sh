@@ -1,0 +1,14 @@
+# full GPU check: tests, smoke, bench, ncu launch list + one --set full capture
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+TAG=${TAG:-r01}
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke_$TAG.log
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_$TAG.log
+timeout 600 python bench.py > gpurun_out/bench_$TAG.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_$TAG.log
+B="python bench.py --ncu --steps 1 --warmup 0 --nsteps 3"
+$B > gpurun_out/ncu_plain_$TAG.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stream -s 1 -c 1 -o gpurun_out/prof_c4_$TAG $B > gpurun_out/ncu_full_$TAG.log 2>&1
+L="python bench.py --steps 3 --warmup 3 --no-cpu"
+$L > gpurun_out/launch_plain_$TAG.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4_$TAG.csv $L > gpurun_out/ncu_launch_$TAG.log 2>&1
+echo done
