@@ -143,6 +143,32 @@ int rtm_kernel_stats(rtm_ctx* ctx, long long* launches, double* total_ms);
 /* Stencil launches issued by the library since creation (all kernels of the step). */
 long long rtm_launch_count(rtm_ctx* ctx);
 
+/* ---- the paper's two-phase blocksize tuner, GPU analogue ----------
+ * PAPER.md:112-126 ("A Framework for Profiling Technique"): a selection phase times every
+ * candidate for nI iterations of the kernel and keeps the best (MinTime); a verification
+ * phase re-times the winner (ActualTime); PAPER.md:276-281 rates the choice by
+ * 100*(ActualTime - MinTime)/MinTime.  Candidates are (tile variant, z-chunk) pairs timed on
+ * the context's real grid with all SMs busy.  With several slabs/ranks a candidate's time is
+ * the worst over ranks and the winner minimises it — the MWMB rule, Eq. (2),
+ * the paper's best procedure.  The wavefield, step counter and the
+ * previous tile/z-chunk settings are restored afterwards (device snapshot; needs 2 extra
+ * fields of device memory); the winner is installed.  Requires a velocity.
+ * tiles/zchunks: ncand pairs; tiles == NULL -> every non-naive variant with z-chunk 0 (auto).
+ * cand_ms (optional, ncand or rtm_num_tiles()-1 doubles) receives each candidate's time. */
+typedef struct {
+    int best_tile;
+    int best_zchunk;
+    int ncandidates;
+    double min_time_ms;     /* MinTime: the winner's selection-phase time for nI steps      */
+    double actual_time_ms;  /* ActualTime: verification-phase time of the winner (nI steps) */
+    double quality_pct;     /* 100 * (ActualTime - MinTime) / MinTime        */
+} rtm_tune_result;
+int rtm_autotune(rtm_ctx* ctx, int nI, const int* tiles, const int* zchunks, int ncand,
+                 rtm_tune_result* out, double* cand_ms);
+/* MWMB selection (host-only): times[r*ncand + c] = time of candidate c on rank r; returns the
+ * c minimising max_r times[r][c] (ties -> lowest c), or -1 on invalid input. */
+int rtm_select_mwmb(const double* times, int nranks, int ncand);
+
 /* ---- z-slab decomposition -------------------------------------------- */
 
 /* One process, several slabs: the grid is split into nslabs z-slabs, slab r on CUDA device

@@ -1014,6 +1014,161 @@ long long rtm_get_option(rtm_ctx* c, int key) {
     }
 }
 
+int rtm_select_mwmb(const double* times, int nranks, int ncand) {
+    if (!times || nranks < 1 || ncand < 1) return -1;
+    int best = -1;
+    double bestv = 0;
+    for (int cnd = 0; cnd < ncand; ++cnd) {
+        double worst = -1e300;
+        bool failed = false;
+        for (int r = 0; r < nranks; ++r) {
+            const double t = times[(size_t)r * ncand + cnd];
+            if (std::isnan(t)) failed = true;  // the candidate failed somewhere
+            else worst = std::max(worst, t);
+        }
+        if (failed) continue;
+        if (best < 0 || worst < bestv) best = cnd, bestv = worst;
+    }
+    return best;
+}
+
+namespace {
+
+// Time nI steps (after one warm-up step) on the context's streams; in a distributed context
+// the result is the max over ranks (NCCL all-reduce).
+int timed_steps(rtm_ctx* c, int nI, double* ms_out, double* d_scratch) {
+    RET(rtm_step(c, 1));
+    RET(rtm_step(c, nI));
+    double ms = c->last_ms;
+    if (c->comm) {
+        Slab& s = c->slabs[0];
+        CK(cudaMemcpyAsync(d_scratch, &ms, sizeof(double), cudaMemcpyHostToDevice, s.stream()));
+        NK(ncclAllReduce(d_scratch, d_scratch, 1, ncclFloat64, ncclMax, c->comm, s.stream()));
+        CK(cudaMemcpyAsync(&ms, d_scratch, sizeof(double), cudaMemcpyDeviceToHost, s.stream()));
+        CK(cudaStreamSynchronize(s.stream()));
+    }
+    *ms_out = ms;
+    return RTM_OK;
+}
+
+}  // namespace
+
+int rtm_autotune(rtm_ctx* c, int nI, const int* tiles, const int* zchunks, int ncand,
+                 rtm_tune_result* out, double* cand_ms) {
+    if (!c || !out) return fail(RTM_EINVAL, "NULL argument");
+    if (nI < 1) return fail(RTM_EINVAL, "nI must be >= 1");
+    if (!c->vel_set) return fail(RTM_ESTATE, "rtm_autotune before a successful rtm_set_velocity");
+    std::vector<int> ct, cz;
+    if (tiles) {
+        if (ncand < 1) return fail(RTM_EINVAL, "ncand must be >= 1");
+        for (int k = 0; k < ncand; ++k) {
+            if (tiles[k] < 0 || tiles[k] >= num_variants())
+                return fail(RTM_EINVAL, "candidate %d: unknown tile %d", k, tiles[k]);
+            if (tiles[k] > 0 && c->nx % 4 != 0)
+                return fail(RTM_EINVAL, "candidate %d: tiled variants need nx %% 4 == 0", k);
+            const int z = zchunks ? zchunks[k] : 0;
+            if (z < 0) return fail(RTM_EINVAL, "candidate %d: z-chunk %d < 0", k, z);
+            ct.push_back(tiles[k]);
+            cz.push_back(z);
+        }
+    } else if (c->nx % 4 != 0) {  // only the naive kernel handles nx % 4 != 0
+        ct.push_back(0);
+        cz.push_back(0);
+    } else {
+        for (int t = 1; t < num_variants(); ++t) {
+            ct.push_back(t);
+            cz.push_back(0);
+        }
+    }
+    DeviceGuard g;
+    const int saved_tile = c->tile, saved_zc = c->zchunk;
+    const long long saved_step = c->step;
+    // snapshot both time levels + step counters of every slab
+    std::vector<float*> snap(2 * c->slabs.size(), nullptr);
+    std::vector<int> snap_step(2 * c->slabs.size());
+    double* d_scratch = nullptr;
+    int rc = RTM_OK;
+    auto cleanup = [&]() {
+        for (size_t k = 0; k < c->slabs.size(); ++k) {
+            cudaSetDevice(c->slabs[k].dev);
+            for (int b = 0; b < 2; ++b)
+                if (snap[2 * k + b]) cudaFree(snap[2 * k + b]);
+        }
+        if (d_scratch) cudaFree(d_scratch);
+    };
+    for (size_t k = 0; k < c->slabs.size() && rc == RTM_OK; ++k) {
+        Slab& s = c->slabs[k];
+        cudaSetDevice(s.dev);
+        const size_t bytes = (size_t)c->nx * c->ny * (s.nzl + 10) * sizeof(float);
+        for (int b = 0; b < 2 && rc == RTM_OK; ++b) {
+            if (cudaMalloc(&snap[2 * k + b], bytes) != cudaSuccess) {
+                cudaGetLastError();
+                rc = fail(RTM_ENOMEM, "autotune snapshot allocation (%zu bytes) failed", bytes);
+                break;
+            }
+            if (cudaMemcpyAsync(snap[2 * k + b], s.buf[b], bytes, cudaMemcpyDeviceToDevice,
+                                s.stream()) != cudaSuccess)
+                rc = fail(RTM_ECUDA, "autotune snapshot copy failed");
+        }
+        if (rc == RTM_OK &&
+            cudaMemcpyAsync(&snap_step[2 * k], s.d_step, 2 * sizeof(int), cudaMemcpyDeviceToHost,
+                            s.stream()) != cudaSuccess)
+            rc = fail(RTM_ECUDA, "autotune step-counter snapshot failed");
+    }
+    if (rc == RTM_OK && c->comm) {
+        cudaSetDevice(c->slabs[0].dev);
+        if (cudaMalloc(&d_scratch, sizeof(double)) != cudaSuccess) rc = fail(RTM_ENOMEM, "scratch");
+    }
+    if (rc == RTM_OK) rc = sync_all(c);
+    std::vector<double> times(ct.size(), std::nan(""));
+    for (size_t k = 0; k < ct.size() && rc == RTM_OK; ++k) {  // selection phase
+        c->tile = ct[k];
+        c->zchunk = cz[k];
+        invalidate_graphs(c);
+        rc = timed_steps(c, nI, &times[k], d_scratch);
+    }
+    int best = -1;
+    if (rc == RTM_OK) {
+        best = rtm_select_mwmb(times.data(), 1, (int)times.size());  // times are already max over ranks
+        if (best < 0) rc = fail(RTM_ECUDA, "no candidate could be timed");
+    }
+    double actual = 0;
+    if (rc == RTM_OK) {  // verification phase
+        c->tile = ct[best];
+        c->zchunk = cz[best];
+        invalidate_graphs(c);
+        rc = timed_steps(c, nI, &actual, d_scratch);
+    }
+    // restore the wavefield and step counter (always, even on failure)
+    for (size_t k = 0; k < c->slabs.size(); ++k) {
+        Slab& s = c->slabs[k];
+        cudaSetDevice(s.dev);
+        const size_t bytes = (size_t)c->nx * c->ny * (s.nzl + 10) * sizeof(float);
+        for (int b = 0; b < 2; ++b)
+            if (snap[2 * k + b])
+                cudaMemcpyAsync(s.buf[b], snap[2 * k + b], bytes, cudaMemcpyDeviceToDevice, s.stream());
+        cudaMemcpyAsync(s.d_step, &snap_step[2 * k], 2 * sizeof(int), cudaMemcpyHostToDevice, s.stream());
+        cudaStreamSynchronize(s.stream());
+    }
+    c->step = saved_step;
+    cleanup();
+    if (rc != RTM_OK) {
+        c->tile = saved_tile;
+        c->zchunk = saved_zc;
+        invalidate_graphs(c);
+        return rc;
+    }
+    out->best_tile = ct[best];
+    out->best_zchunk = cz[best];
+    out->ncandidates = (int)ct.size();
+    out->min_time_ms = times[best];
+    out->actual_time_ms = actual;
+    out->quality_pct = 100.0 * (actual - times[best]) / times[best];
+    if (cand_ms)
+        for (size_t k = 0; k < times.size(); ++k) cand_ms[k] = times[k];
+    return RTM_OK;
+}
+
 int rtm_set_stream(rtm_ctx* c, void* stream) {
     if (!c) return fail(RTM_EINVAL, "ctx is NULL");
     if (c->slabs.size() != 1)

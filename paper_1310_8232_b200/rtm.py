@@ -34,6 +34,12 @@ if not _LIB_PATH.exists():
 lib = ctypes.CDLL(str(_LIB_PATH))
 
 _P, _I, _F, _D, _LL = ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.c_double, ctypes.c_longlong
+
+
+class rtm_tune_result(ctypes.Structure):
+    _fields_ = [("best_tile", ctypes.c_int), ("best_zchunk", ctypes.c_int),
+                ("ncandidates", ctypes.c_int), ("min_time_ms", ctypes.c_double),
+                ("actual_time_ms", ctypes.c_double), ("quality_pct", ctypes.c_double)]
 _SIGS = {
     "rtm_create": (_P, [_I, _I, _I, _F, _F, _P]),
     "rtm_set_velocity": (_I, [_P, _P]),
@@ -66,6 +72,8 @@ _SIGS = {
     "rtm_slab_range": (_I, [_I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "rtm_halo_plan": (_I, [_I, _I, _I, _I, _I, ctypes.POINTER(_LL), ctypes.POINTER(_LL)]),
     "rtm_nu_crit": (_D, [_P]),
+    "rtm_autotune": (_I, [_P, _I, _P, _P, _I, ctypes.POINTER(rtm_tune_result), _P]),
+    "rtm_select_mwmb": (_I, [_P, _I, _I]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)
@@ -263,3 +271,28 @@ def rtm_halo_plan(nx, ny, nzl, rank, world):
 
 def rtm_nu_crit(coeffs) -> float:
     return float(lib.rtm_nu_crit(_ptr(_coeffs(coeffs))))
+
+
+def rtm_autotune(h, nI, tiles=None, zchunks=None):
+    """Two-phase selection/verification tuner.  Returns (result dict,
+    per-candidate selection times in ms)."""
+    res = rtm_tune_result()
+    if tiles is not None:
+        t = np.ascontiguousarray(tiles, dtype=np.int32)
+        z = np.ascontiguousarray(zchunks if zchunks is not None else np.zeros(len(t)), dtype=np.int32)
+        n = len(t)
+    else:
+        t = z = None
+        n = rtm_num_tiles()
+    times = np.full(n, np.nan)
+    _check(lib.rtm_autotune(h, int(nI), _ptr(t), _ptr(z), int(n if t is not None else 0),
+                            ctypes.byref(res), _ptr(times)))
+    d = {f: getattr(res, f) for f, _ in rtm_tune_result._fields_}
+    return d, times[: res.ncandidates]
+
+
+def rtm_select_mwmb(times) -> int:
+    t = np.ascontiguousarray(times, dtype=np.float64)
+    if t.ndim != 2:
+        raise ValueError("times must be (nranks, ncand)")
+    return int(lib.rtm_select_mwmb(_ptr(t), int(t.shape[0]), int(t.shape[1])))

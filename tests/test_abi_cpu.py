@@ -120,3 +120,19 @@ def test_sass_has_tma_and_no_legacy_tensor_ops():
     assert "UTMALDG" in sass
     assert "SYNCS" in sass  # mbarrier operations
     assert "HMMA" not in sass
+
+
+def test_select_mwmb_is_eq2_minmax(P):
+    """MWMB (Eq. (2)): per candidate the worst time over processes, then
+    the candidate with the smallest worst case.  Differs from min-of-min (MMMB, Eq. (1))."""
+    t = np.array([[1.0, 2.0, 3.0],     # rank 0
+                  [9.0, 2.5, 2.9]])    # rank 1: candidate 0 is fast on rank 0 only
+    assert P.rtm_select_mwmb(t) == 1            # max = (9, 2.5, 3.0) -> candidate 1
+    assert int(np.argmin(t.min(axis=0))) == 0    # MMMB would pick candidate 0
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        m = rng.uniform(1, 10, (rng.integers(1, 9), rng.integers(1, 20)))
+        assert P.rtm_select_mwmb(m) == int(np.argmin(m.max(axis=0)))
+    m = np.array([[np.nan, 5.0, 4.0], [1.0, 4.0, 6.0]])
+    assert P.rtm_select_mwmb(m) == 1  # a candidate that failed anywhere is never chosen
+    assert P.rtm_select_mwmb(np.array([[2.0, 2.0]])) == 0  # ties -> lowest index

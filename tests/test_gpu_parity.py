@@ -372,3 +372,41 @@ def test_device_pointer_variants_and_user_stream(P):
         n, ms = P.rtm_kernel_stats(sim.h)
         assert n == 5 and ms > 0
         P.rtm_set_stream(sim.h, 0)
+
+
+# ----------------------------------------------------------------------------- tuner (f2)
+def test_autotune_preserves_state_and_installs_winner(P):
+    cfg = ri.make_config(2, shape=(96, 128, 128), steps=30)
+    v = cfg.velocity()
+    src = cfg.sources()
+    ref = gpu_run(P, v, cfg.dx, cfg.dt, 30, sources=src)
+    with P.Simulation(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, C32) as sim:
+        sim.set_velocity(v)
+        for s in src:
+            sim.inject_source(*s)
+        sim.step(11)
+        res, times = P.rtm_autotune(sim.h, 4)
+        assert res["ncandidates"] == P.rtm_num_tiles() - 1 and len(times) == res["ncandidates"]
+        assert np.all(np.isfinite(times)) and np.all(times > 0)
+        assert res["min_time_ms"] == pytest.approx(times.min())
+        assert res["quality_pct"] == pytest.approx(
+            100 * (res["actual_time_ms"] - res["min_time_ms"]) / res["min_time_ms"])
+        assert sim.tile == res["best_tile"] and sim.steps_taken == 11
+        sim.step(19)
+        assert np.array_equal(sim.read_field(), ref)
+        res2, t2 = P.rtm_autotune(sim.h, 2, tiles=[1, 1, 2], zchunks=[0, 7, 0])
+        assert res2["ncandidates"] == 3 and res2["best_tile"] in (1, 2)
+
+
+def test_autotune_multislab(P):
+    nz, ny, nx = 60, 40, 64
+    v = np.full((nz, ny, nx), 2500.0, np.float32)
+    u0, up0 = ri.random_fields(v.shape, seed=4)
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, devices=[0, 0]) as sim:
+        sim.set_velocity(v)
+        sim.set_fields(u0, up0)
+        res, times = P.rtm_autotune(sim.h, 2, tiles=[1, 5, 0])
+        assert res["best_tile"] in (1, 5)  # the naive kernel is never the fastest
+        sim.step(4)
+        got = sim.read_field()
+    assert np.array_equal(got, gpu_run(P, v, 10.0, 1e-3, 4, u0=u0, up0=up0))

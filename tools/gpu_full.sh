@@ -2,9 +2,12 @@
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 TAG=${TAG:-r01}
+nvidia-smi --query-gpu=name,clocks.max.sm,clocks.mem,power.limit --format=csv > gpurun_out/gpu_$TAG.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke_$TAG.log
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_$TAG.log
 timeout 600 python bench.py > gpurun_out/bench_$TAG.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_$TAG.log
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_$TAG.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref_$TAG.log
+for c in 3 5 2 1; do timeout 600 python bench.py --config $c --no-cpu > gpurun_out/bench_c${c}_$TAG.log 2>&1; done
 B="python bench.py --ncu --steps 1 --warmup 0 --nsteps 3"
 $B > gpurun_out/ncu_plain_$TAG.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stream -s 1 -c 1 -o gpurun_out/prof_c4_$TAG $B > gpurun_out/ncu_full_$TAG.log 2>&1

@@ -39,5 +39,31 @@ def summary(rep):
     return res
 
 
+def _num(v):
+    return float(v.split()[0])
+
+
+def _scale(v):
+    num, unit = v.split()[0], (v.split()[1] if len(v.split()) > 1 else "")
+    f = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1)
+    return float(num) * f
+
+
 if __name__ == "__main__":
-    print(json.dumps(summary(sys.argv[1]), indent=1))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("rep")
+    ap.add_argument("--workload", default=None)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    res = summary(a.rep)
+    if a.workload:  # bench-consumable record for the dominant (first) kernel
+        k = res[0]
+        rd, wr = _scale(k["dram__bytes_read.sum"]), _scale(k["dram__bytes_write.sum"])
+        res = {"workload": a.workload, "report": a.rep.split("/")[-1], "kernel": k["kernel"],
+               "dram_bytes_per_launch": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
+               "duration_ms": _num(k["gpu__time_duration.sum"]), "detail": k}
+    txt = json.dumps(res, indent=1)
+    if a.out:
+        open(a.out, "w").write(txt + "\n")
+    print(txt)
