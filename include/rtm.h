@@ -169,6 +169,20 @@ int rtm_autotune(rtm_ctx* ctx, int nI, const int* tiles, const int* zchunks, int
  * c minimising max_r times[r][c] (ties -> lowest c), or -1 on invalid input. */
 int rtm_select_mwmb(const double* times, int nranks, int ncand);
 
+/* ---- batched shots (the paper's production mode runs one independent
+ * grid per process) ------------------------------------------------
+ * One context, nshots independent wavefields on one velocity model (RTM shots share the
+ * model, differ in sources).  Host field arrays become (nshots, nz, ny, nx); the velocity stays
+ * (nz, ny, nx).  Work units are dealt shot-fastest, so co-running CTAs read the same C tile
+ * (one HBM read serves all shots through L2).  rtm_inject_source registers on shot 0;
+ * rtm_inject_source_shot on any shot (the RTM_MAX_SOURCES limit is per context).
+ * Single-GPU only; across GPUs run one batch per GPU (replicas, no exchange). */
+rtm_ctx* rtm_create_batch(int nx, int ny, int nz, float dx, float dt, const float coeffs[6],
+                          int nshots);
+int rtm_num_shots(rtm_ctx* ctx);
+int rtm_inject_source_shot(rtm_ctx* ctx, int shot, int ix, int iy, int iz, const float* samples,
+                           int nsamples);
+
 /* ---- z-slab decomposition -------------------------------------------- */
 
 /* One process, several slabs: the grid is split into nslabs z-slabs, slab r on CUDA device

@@ -19,10 +19,14 @@ __all__ = ["Simulation", "RtmError"] + [n for n in dir(_r) if n.startswith(("rtm
 class Simulation:
     """Owns one rtm_ctx.  Arrays are float32 (nz, ny, nx)."""
 
-    def __init__(self, nx, ny, nz, dx, dt, coeffs, *, devices=None, dist=None):
+    def __init__(self, nx, ny, nz, dx, dt, coeffs, *, devices=None, dist=None, shots=1):
         self.nx, self.ny, self.nz = int(nx), int(ny), int(nz)
         self.dist = dist
-        if dist is not None:  # (rank, world, uid, device)
+        self.shots = int(shots)
+        if self.shots > 1:  # batched independent wavefields on one velocity model
+            self.h = _r.rtm_create_batch(nx, ny, nz, dx, dt, coeffs, self.shots)
+            self.z0, self.nzl = 0, self.nz
+        elif dist is not None:  # (rank, world, uid, device)
             rank, world, uid, device = dist
             self.h = _r.rtm_create_dist(nx, ny, nz, dx, dt, coeffs, rank, world, uid, device)
             self.z0, self.nzl = _r.rtm_slab_range(nz, world, rank)
@@ -35,13 +39,15 @@ class Simulation:
 
     @property
     def local_shape(self):
+        if self.shots > 1:
+            return (self.shots, self.nzl, self.ny, self.nx)
         return (self.nzl, self.ny, self.nx)
 
     def set_velocity(self, v):
         _r.rtm_set_velocity(self.h, v, n=self.nx * self.ny * self.nzl)
 
-    def inject_source(self, ix, iy, iz, samples):
-        _r.rtm_inject_source(self.h, ix, iy, iz, samples)
+    def inject_source(self, ix, iy, iz, samples, shot=0):
+        _r.rtm_inject_source_shot(self.h, shot, ix, iy, iz, samples)
 
     def set_fields(self, u=None, u_prev=None):
         _r.rtm_set_fields(self.h, u, u_prev)

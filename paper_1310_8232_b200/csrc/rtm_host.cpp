@@ -67,6 +67,7 @@ struct DeviceGuard {  // restore the caller's current device
 
 struct HostSource {
     int x, y, z;  // global
+    int shot;
     std::vector<float> samples;
 };
 
@@ -75,8 +76,10 @@ constexpr int GRAPH_PAIRS = 8;  // a captured graph advances 2*GRAPH_PAIRS steps
 struct Slab {
     int dev = 0;
     int z0 = 0, nzl = 0;
+    int nshots = 1;                      // batched independent wavefields sharing C
     bool lo_nb = false, hi_nb = false;
-    float* buf[2] = {nullptr, nullptr};  // nzl+10 planes each
+    float* buf[2] = {nullptr, nullptr};  // nshots*(nzl+10) planes each
+    size_t buf_planes() const { return (size_t)nshots * (nzl + 10); }
     float* C = nullptr;                  // nzl planes
     int* d_step = nullptr;               // [2]
     unsigned int* d_stats = nullptr;     // [2] velocity check
@@ -187,7 +190,7 @@ int validate_grid(int nx, int ny, int nz, float dx, float dt, const float* coeff
 int alloc_slab(rtm_ctx* c, Slab& s) {
     CK(cudaSetDevice(s.dev));
     const size_t plane = (size_t)c->nx * c->ny;
-    const size_t nbuf = plane * (s.nzl + 10);
+    const size_t nbuf = plane * s.buf_planes();
     for (int b = 0; b < 2; ++b) {
         if (cudaMalloc(&s.buf[b], nbuf * sizeof(float)) != cudaSuccess) {
             cudaGetLastError();
@@ -308,8 +311,9 @@ int ensure_tmaps(rtm_ctx* c, Slab& s, int var) {
     if (var == 0 || s.tm_variant == key) return RTM_OK;
     const TileVariant& tv = variant(var);
     for (int b = 0; b < 2; ++b) {
-        RET(encode_3d(&s.tm_u[b], s.buf[b], c->nx, c->ny, s.nzl + 10, tv.TX + 16, tv.TY + 10, promo));
-        RET(encode_3d(&s.tm_in[b], s.buf[b], c->nx, c->ny, s.nzl + 10, tv.TX, tv.TY));
+        RET(encode_3d(&s.tm_u[b], s.buf[b], c->nx, c->ny, (int)s.buf_planes(), tv.TX + 16,
+                      tv.TY + 10, promo));
+        RET(encode_3d(&s.tm_in[b], s.buf[b], c->nx, c->ny, (int)s.buf_planes(), tv.TX, tv.TY));
     }
     RET(encode_3d(&s.tm_c, s.C, c->nx, c->ny, s.nzl, tv.TX, tv.TY));
     int tpb = 0;
@@ -344,6 +348,7 @@ void fill_params(const rtm_ctx* c, const Slab& s, int parity, StencilParams& p) 
     p.nx = c->nx;
     p.ny = c->ny;
     p.nzl = s.nzl;
+    p.nshots = s.nshots;
     p.plane = (long long)c->nx * c->ny;
     p.coef[0] = 3.0f * c->coeffs[0];
     for (int k = 1; k < 6; ++k) p.coef[k] = c->coeffs[k];
@@ -632,11 +637,15 @@ int reset_impl(rtm_ctx* c, const float* u, const float* up) {
         CK(cudaSetDevice(s.dev));
         cudaStream_t st = s.stream();
         CK(cudaStreamSynchronize(s.s_comm));
-        const size_t nbuf = plane * (s.nzl + 10);
+        const size_t nbuf = plane * s.buf_planes();
         for (int b = 0; b < 2; ++b) CK(cudaMemsetAsync(s.buf[b], 0, nbuf * sizeof(float), st));
         const size_t off = c->mode == 1 ? (size_t)s.z0 * plane : 0;
-        if (u) RET(h2d_planes(c, s, s.buf[0] + 5 * plane, u + off, st));
-        if (up) RET(h2d_planes(c, s, s.buf[1] + 5 * plane, up + off, st));
+        for (int k = 0; k < s.nshots; ++k) {  // host arrays: (nshots, nz, ny, nx)
+            const size_t hoff = off + (size_t)k * plane * s.nzl;
+            const size_t doff = ((size_t)k * (s.nzl + 10) + 5) * plane;
+            if (u) RET(h2d_planes(c, s, s.buf[0] + doff, u + hoff, st));
+            if (up) RET(h2d_planes(c, s, s.buf[1] + doff, up + hoff, st));
+        }
         CK(cudaMemsetAsync(s.d_step, 0, 2 * sizeof(int), st));
     }
     c->step = 0;
@@ -660,8 +669,10 @@ int read_impl(rtm_ctx* c, float* out, int which /*0 = u^n, 1 = u^{n-1}*/) {
     for (auto& s : c->slabs) {
         CK(cudaSetDevice(s.dev));
         const size_t off = c->mode == 1 ? (size_t)s.z0 * plane : 0;
-        CK(cudaMemcpyAsync(out + off, s.buf[par] + 5 * plane, plane * s.nzl * sizeof(float),
-                           cudaMemcpyDeviceToHost, s.stream()));
+        for (int k = 0; k < s.nshots; ++k)
+            CK(cudaMemcpyAsync(out + off + (size_t)k * plane * s.nzl,
+                               s.buf[par] + ((size_t)k * (s.nzl + 10) + 5) * plane,
+                               plane * s.nzl * sizeof(float), cudaMemcpyDeviceToHost, s.stream()));
     }
     return sync_all(c);
 }
@@ -730,6 +741,37 @@ rtm_ctx* rtm_create(int nx, int ny, int nz, float dx, float dt, const float coef
     }
     return c;
 }
+
+rtm_ctx* rtm_create_batch(int nx, int ny, int nz, float dx, float dt, const float coeffs[6],
+                          int nshots) {
+    DeviceGuard g;
+    if (nshots < 1) {
+        fail(RTM_EINVAL, "nshots must be >= 1");
+        return nullptr;
+    }
+    if ((long long)nshots * (nz + 10) > (1LL << 31) - 1) {
+        fail(RTM_EINVAL, "nshots*(nz+10) = %lld planes exceeds 2^31", (long long)nshots * (nz + 10));
+        return nullptr;
+    }
+    rtm_ctx* c = new_ctx(nx, ny, nz, dx, dt, coeffs);
+    if (!c) return nullptr;
+    c->mode = 0;
+    Slab s;
+    cudaGetDevice(&s.dev);
+    s.z0 = 0;
+    s.nzl = nz;
+    s.nshots = nshots;
+    c->slabs.push_back(s);
+    if (finish_ctx(c) != RTM_OK) {
+        std::string e = g_err;
+        destroy_ctx(c);
+        g_err = e;
+        return nullptr;
+    }
+    return c;
+}
+
+int rtm_num_shots(rtm_ctx* c) { return c ? c->slabs[0].nshots : -1; }
 
 rtm_ctx* rtm_create_multi(int nx, int ny, int nz, float dx, float dt, const float coeffs[6],
                           int nslabs, const int* devices) {
@@ -852,8 +894,11 @@ int rtm_set_velocity_device(rtm_ctx* c, const float* d_v) {
     return set_velocity_impl(c, d_v, true);
 }
 
-int rtm_inject_source(rtm_ctx* c, int ix, int iy, int iz, const float* samples, int nsamples) {
+int rtm_inject_source_shot(rtm_ctx* c, int shot, int ix, int iy, int iz, const float* samples,
+                           int nsamples) {
     if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    if (shot < 0 || shot >= c->slabs[0].nshots)
+        return fail(RTM_EINVAL, "shot %d outside [0, %d)", shot, c->slabs[0].nshots);
     if (ix < 0 || ix >= c->nx || iy < 0 || iy >= c->ny || iz < 0 || iz >= c->nz)
         return fail(RTM_EINVAL, "source (%d,%d,%d) outside the %dx%dx%d interior", ix, iy, iz,
                     c->nx, c->ny, c->nz);
@@ -864,7 +909,7 @@ int rtm_inject_source(rtm_ctx* c, int ix, int iy, int iz, const float* samples, 
     if ((int)c->sources.size() >= RTM_MAX_SOURCES)
         return fail(RTM_EINVAL, "at most %d sources", RTM_MAX_SOURCES);
     DeviceGuard g;
-    HostSource hs{ix, iy, iz, std::vector<float>(samples, samples + nsamples)};
+    HostSource hs{ix, iy, iz, shot, std::vector<float>(samples, samples + nsamples)};
     c->sources.push_back(hs);
     for (auto& s : c->slabs) {
         if (iz < s.z0 || iz >= s.z0 + s.nzl) continue;  // owned by another slab / rank
@@ -872,6 +917,7 @@ int rtm_inject_source(rtm_ctx* c, int ix, int iy, int iz, const float* samples, 
         d.x = ix;
         d.y = iy;
         d.z = iz - s.z0;
+        d.shot = shot;
         d.nsamples = nsamples;
         d.offset = (long long)s.h_samples.size();
         s.h_samples.insert(s.h_samples.end(), samples, samples + nsamples);
@@ -879,6 +925,10 @@ int rtm_inject_source(rtm_ctx* c, int ix, int iy, int iz, const float* samples, 
         RET(upload_sources(c, s));
     }
     return RTM_OK;
+}
+
+int rtm_inject_source(rtm_ctx* c, int ix, int iy, int iz, const float* samples, int nsamples) {
+    return rtm_inject_source_shot(c, 0, ix, iy, iz, samples, nsamples);
 }
 
 int rtm_step(rtm_ctx* c, int nsteps) {
@@ -934,8 +984,10 @@ int rtm_read_field_device(rtm_ctx* c, float* d_out) {
     Slab& s = c->slabs[0];
     CK(cudaSetDevice(s.dev));
     const size_t plane = (size_t)c->nx * c->ny;
-    CK(cudaMemcpyAsync(d_out, s.buf[c->step & 1] + 5 * plane, plane * s.nzl * sizeof(float),
-                       cudaMemcpyDeviceToDevice, s.stream()));
+    for (int k = 0; k < s.nshots; ++k)
+        CK(cudaMemcpyAsync(d_out + (size_t)k * plane * s.nzl,
+                           s.buf[c->step & 1] + ((size_t)k * (s.nzl + 10) + 5) * plane,
+                           plane * s.nzl * sizeof(float), cudaMemcpyDeviceToDevice, s.stream()));
     return RTM_OK;
 }
 
@@ -951,7 +1003,7 @@ int rtm_reset(rtm_ctx* c) {
     if (c->mode == 0) {  // enqueue only (the bench times reset inside a step)
         Slab& s = c->slabs[0];
         CK(cudaSetDevice(s.dev));
-        const size_t nbuf = (size_t)c->nx * c->ny * (s.nzl + 10);
+        const size_t nbuf = (size_t)c->nx * c->ny * s.buf_planes();
         for (int b = 0; b < 2; ++b) CK(cudaMemsetAsync(s.buf[b], 0, nbuf * sizeof(float), s.stream()));
         CK(cudaMemsetAsync(s.d_step, 0, 2 * sizeof(int), s.stream()));
         c->step = 0;
@@ -1099,7 +1151,7 @@ int rtm_autotune(rtm_ctx* c, int nI, const int* tiles, const int* zchunks, int n
     for (size_t k = 0; k < c->slabs.size() && rc == RTM_OK; ++k) {
         Slab& s = c->slabs[k];
         cudaSetDevice(s.dev);
-        const size_t bytes = (size_t)c->nx * c->ny * (s.nzl + 10) * sizeof(float);
+        const size_t bytes = (size_t)c->nx * c->ny * s.buf_planes() * sizeof(float);
         for (int b = 0; b < 2 && rc == RTM_OK; ++b) {
             if (cudaMalloc(&snap[2 * k + b], bytes) != cudaSuccess) {
                 cudaGetLastError();
@@ -1143,7 +1195,7 @@ int rtm_autotune(rtm_ctx* c, int nI, const int* tiles, const int* zchunks, int n
     for (size_t k = 0; k < c->slabs.size(); ++k) {
         Slab& s = c->slabs[k];
         cudaSetDevice(s.dev);
-        const size_t bytes = (size_t)c->nx * c->ny * (s.nzl + 10) * sizeof(float);
+        const size_t bytes = (size_t)c->nx * c->ny * s.buf_planes() * sizeof(float);
         for (int b = 0; b < 2; ++b)
             if (snap[2 * k + b])
                 cudaMemcpyAsync(s.buf[b], snap[2 * k + b], bytes, cudaMemcpyDeviceToDevice, s.stream());

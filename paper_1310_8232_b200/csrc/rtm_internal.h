@@ -13,6 +13,7 @@ constexpr int RADIUS = 5;  // "five points (cells) in each direction" (PAPER.md:
 
 struct DevSource {       // a source owned by this slab, LOCAL coordinates
     int x, y, z;         // z = owned plane index (0..nzl-1)
+    int shot;            // wavefield index in a batched (multi-shot) context
     int nsamples;
     long long offset;    // into StencilParams::samples
 };
@@ -21,6 +22,8 @@ struct DevSource {       // a source owned by this slab, LOCAL coordinates
 struct StencilParams {
     int nx, ny, nzl;           // interior extents of this slab
     long long plane;           // nx*ny
+    int nshots;                // independent wavefields sharing C (batched shots); shot k's
+                               // planes start at buffer plane k*(nzl+10)
     float coef[6];             // coef[0] = 3*c0 (fp32, host-folded), coef[1..5] = c1..c5
     const float* u;            // u^n buffer base (nzl+10 planes, plane 0 = first halo plane)
     float* next;               // u^{n-1} buffer base, overwritten in place by u^{n+1}

@@ -143,9 +143,12 @@ __global__ void __launch_bounds__(TX * TY / 4, MINB)
 
     // ---- work unit: (z-chunk, tile), chunk-major so concurrently running CTAs are xy
     // neighbours at similar z (their halo re-reads hit L2)
+    const int shot = blockIdx.x % p.nshots;
+    const int ublk = blockIdx.x / p.nshots;
+    const long long soff = (long long)shot * (p.nzl + 10);
     const int ntiles = p.tiles_x * p.tiles_y;
-    int chunk = blockIdx.x / ntiles;
-    const int tile = blockIdx.x - chunk * ntiles;
+    int chunk = ublk / ntiles;
+    const int tile = ublk - chunk * ntiles;
     int r = 0;
     if (chunk >= p.r_chunks[0]) {
         r = 1;
@@ -172,7 +175,7 @@ __global__ void __launch_bounds__(TX * TY / 4, MINB)
     auto issue = [&](int j) {
         const int slot = j % K;
         mbar_expect_tx(&bars[slot], S::BOX_BYTES);
-        tma_load_3d(ring + slot * S::SLOT, &tm, x0 - 8, y0 - 5, zs + j, &bars[slot]);
+        tma_load_3d(ring + slot * S::SLOT, &tm, x0 - 8, y0 - 5, (int)soff + zs + j, &bars[slot]);
     };
     if (tid == 0) {
         const int first = L < K ? L : K;
@@ -186,7 +189,8 @@ __global__ void __launch_bounds__(TX * TY / 4, MINB)
 #pragma unroll 1
         for (int s = 0; s < p.nsrc; ++s) {
             const DevSource& src = p.src[s];
-            if (src.y == y && src.x >= x && src.x < x + 4 && src.z >= zs && src.z < ze)
+            if (src.shot == shot && src.y == y && src.x >= x && src.x < x + 4 && src.z >= zs &&
+                src.z < ze)
                 smask |= (1ull << s);
         }
     }
@@ -213,7 +217,7 @@ __global__ void __launch_bounds__(TX * TY / 4, MINB)
 
     float4 upv = make_float4(0.f, 0.f, 0.f, 0.f), cv = upv;
     if (active) {
-        upv = ld_stream4(p.next + (long long)(zs + 5) * p.plane + col);
+        upv = ld_stream4(p.next + (soff + zs + 5) * p.plane + col);
         cv = ld_stream4(p.C + (long long)zs * p.plane + col);
     }
     const float c[6] = {p.coef[0], p.coef[1], p.coef[2], p.coef[3], p.coef[4], p.coef[5]};
@@ -223,7 +227,7 @@ __global__ void __launch_bounds__(TX * TY / 4, MINB)
         const int i = z - zs;
         float4 upn = upv, cn = cv;
         if (active && z + 1 < ze) {  // one plane ahead
-            upn = ld_stream4(p.next + (long long)(z + 6) * p.plane + col);
+            upn = ld_stream4(p.next + (soff + z + 6) * p.plane + col);
             cn = ld_stream4(p.C + (long long)(z + 1) * p.plane + col);
         }
         const int jn = i + 10, jc = i + 5;
@@ -263,7 +267,7 @@ __global__ void __launch_bounds__(TX * TY / 4, MINB)
         }
         if (smask) add_sources(p, smask, x, z, out);
         if (active)
-            st_stream4(p.next + (long long)(z + 5) * p.plane + col,
+            st_stream4(p.next + (soff + z + 5) * p.plane + col,
                        make_float4(out[0], out[1], out[2], out[3]));
 
 #pragma unroll
@@ -280,14 +284,16 @@ __global__ void __launch_bounds__(TX * TY / 4, MINB)
 
 // ------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_naive(const __grid_constant__ StencilParams p) {
-    long long total = (long long)p.r_len[0] * p.plane;
-    if (p.nranges > 1) total += (long long)p.r_len[1] * p.plane;
+    long long per_shot = (long long)p.r_len[0] * p.plane;
+    if (p.nranges > 1) per_shot += (long long)p.r_len[1] * p.plane;
+    const long long total = per_shot * p.nshots;
     if (p.write_next && blockIdx.x == 0 && threadIdx.x == 0)
         p.d_step[p.parity ^ 1] = p.d_step[p.parity] + 1;
     const float c[6] = {p.coef[0], p.coef[1], p.coef[2], p.coef[3], p.coef[4], p.coef[5]};
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
          t += (long long)gridDim.x * blockDim.x) {
-        long long tt = t;
+        const int shot = static_cast<int>(t / per_shot);
+        long long tt = t - shot * per_shot;
         int z;
         const long long n0 = (long long)p.r_len[0] * p.plane;
         if (tt < n0) {
@@ -299,7 +305,7 @@ __global__ void __launch_bounds__(256) k_naive(const __grid_constant__ StencilPa
         const long long inplane = tt % p.plane;
         const int y = static_cast<int>(inplane / p.nx);
         const int x = static_cast<int>(inplane - (long long)y * p.nx);
-        const long long pb = (long long)(z + 5) * p.plane + inplane;  // buffer index
+        const long long pb = ((long long)shot * (p.nzl + 10) + z + 5) * p.plane + inplane;  // buffer index
         float zl[11], yl[11], xl[11];
 #pragma unroll
         for (int o = -5; o <= 5; ++o) {
@@ -311,7 +317,7 @@ __global__ void __launch_bounds__(256) k_naive(const __grid_constant__ StencilPa
         float out = rtm_point(zl, yl, xl, p.next[pb], p.C[(long long)z * p.plane + inplane], c);
         for (int s = 0; s < p.nsrc; ++s) {
             const DevSource& src = p.src[s];
-            if (src.x == x && src.y == y && src.z == z) {
+            if (src.x == x && src.y == y && src.z == z && src.shot == shot) {
                 const int n = p.d_step[p.parity];
                 if (n < src.nsamples) out = __fadd_rn(out, p.samples[src.offset + n]);
             }
@@ -430,8 +436,14 @@ __device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* t
 
 struct UnitGeom {
     int x0, y0, zs, ze;
+    int shot;
+    long long soff;  // buffer-plane offset of the shot: shot * (nzl + 10)
 };
+// unit = ((chunk * ntiles) + tile) * nshots + shot: shots fastest (concurrent CTAs share the
+// C tile through L2), then tiles (co-running xy neighbours share halos), then z-chunks.
 __device__ __forceinline__ UnitGeom unit_geom(const StencilParams& p, int unit, int TX, int TY) {
+    const int shot = unit % p.nshots;
+    unit /= p.nshots;
     const int ntiles = p.tiles_x * p.tiles_y;
     int chunk = unit / ntiles;
     const int tile = unit - chunk * ntiles;
@@ -446,6 +458,8 @@ __device__ __forceinline__ UnitGeom unit_geom(const StencilParams& p, int unit, 
     const int tyi = tile / p.tiles_x;
     g.x0 = (tile - tyi * p.tiles_x) * TX;
     g.y0 = tyi * TY;
+    g.shot = shot;
+    g.soff = (long long)shot * (p.nzl + 10);
     return g;
 }
 
@@ -479,7 +493,8 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
         p.d_step[p.parity ^ 1] = p.d_step[p.parity] + 1;
     __syncthreads();
 
-    const int units = p.tiles_x * p.tiles_y * (p.r_chunks[0] + (p.nranges > 1 ? p.r_chunks[1] : 0));
+    const int units = p.tiles_x * p.tiles_y * (p.r_chunks[0] + (p.nranges > 1 ? p.r_chunks[1] : 0)) *
+                      p.nshots;
 
     if (warp == S::NW) {  // ---------------- producer warp
         if (lane == 0) {
@@ -495,17 +510,17 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
                     mbar_expect_tx(&full_u[slot], S::UBYTES);
                     if (hint)
                         tma_load_3d_hint(uring + slot * S::USLOT, &tm_u, g.x0 - 8, g.y0 - 5,
-                                         g.zs + j, &full_u[slot], pol);
+                                         (int)g.soff + g.zs + j, &full_u[slot], pol);
                     else
-                        tma_load_3d(uring + slot * S::USLOT, &tm_u, g.x0 - 8, g.y0 - 5, g.zs + j,
-                                    &full_u[slot]);
+                        tma_load_3d(uring + slot * S::USLOT, &tm_u, g.x0 - 8, g.y0 - 5,
+                                    (int)g.soff + g.zs + j, &full_u[slot]);
                 };
                 auto put_c = [&](int i) {
                     const uint32_t seq = gc + i, slot = seq % D;
                     if (seq >= D) mbar_wait(&empty_c[slot], ((seq / D) - 1) & 1);
                     mbar_expect_tx(&full_c[slot], S::CBYTES);
                     float* dst = cring + slot * S::CSLOT;
-                    tma_load_3d(dst, &tm_up, g.x0, g.y0, g.zs + i + 5, &full_c[slot]);
+                    tma_load_3d(dst, &tm_up, g.x0, g.y0, (int)g.soff + g.zs + i + 5, &full_c[slot]);
                     tma_load_3d(dst + TX * TY, &tm_c, g.x0, g.y0, g.zs + i, &full_c[slot]);
                 };
                 for (int j = 0; j < 10; ++j) put_u(j);
@@ -542,12 +557,13 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
         if (active) {
             for (int s = 0; s < p.nsrc; ++s) {
                 const DevSource& src = p.src[s];
-                if (src.y == y && src.x >= x && src.x < x + 4 && src.z >= g.zs && src.z < g.ze)
+                if (src.shot == g.shot && src.y == y && src.x >= x && src.x < x + 4 &&
+                    src.z >= g.zs && src.z < g.ze)
                     smask |= (1ull << s);
             }
         }
         const long long col = (long long)y * p.nx + x;
-        float* outp = p.next + (long long)(g.zs + 5) * p.plane + col;  // also u_prev (D == 0)
+        float* outp = p.next + (g.soff + g.zs + 5) * p.plane + col;  // also u_prev (D == 0)
         const float* cp = p.C + (long long)g.zs * p.plane + col;
 
         float4 q[11];
@@ -723,7 +739,7 @@ cudaError_t launch_variant(int id, const CUtensorMap* tm_u, const CUtensorMap* t
     cudaError_t e = variant_fn(id, &fn, &threads, &smem);
     if (e != cudaSuccess) return e;
     const long long units = (long long)p.tiles_x * p.tiles_y *
-                            (p.r_chunks[0] + (p.nranges > 1 ? p.r_chunks[1] : 0));
+                            (p.r_chunks[0] + (p.nranges > 1 ? p.r_chunks[1] : 0)) * p.nshots;
     if (units <= 0) return cudaSuccess;
     if (variant(id).kind == 1) {
         void* args[] = {const_cast<CUtensorMap*>(tm_u), const_cast<StencilParams*>(&p)};
@@ -738,6 +754,7 @@ cudaError_t launch_variant(int id, const CUtensorMap* tm_u, const CUtensorMap* t
 cudaError_t launch_naive(const StencilParams& p, cudaStream_t s) {
     long long total = (long long)p.r_len[0] * p.plane;
     if (p.nranges > 1) total += (long long)p.r_len[1] * p.plane;
+    total *= p.nshots;
     if (total <= 0) return cudaSuccess;
     long long blocks = (total + 255) / 256;
     if (blocks > 148LL * 64) blocks = 148LL * 64;

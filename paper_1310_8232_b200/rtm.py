@@ -67,6 +67,9 @@ _SIGS = {
     "rtm_kernel_stats": (_I, [_P, ctypes.POINTER(_LL), ctypes.POINTER(_D)]),
     "rtm_launch_count": (_LL, [_P]),
     "rtm_create_multi": (_P, [_I, _I, _I, _F, _F, _P, _I, _P]),
+    "rtm_create_batch": (_P, [_I, _I, _I, _F, _F, _P, _I]),
+    "rtm_num_shots": (_I, [_P]),
+    "rtm_inject_source_shot": (_I, [_P, _I, _I, _I, _I, _P, _I]),
     "rtm_get_unique_id": (_I, [_P]),
     "rtm_create_dist": (_P, [_I, _I, _I, _F, _F, _P, _I, _I, _P, _I]),
     "rtm_slab_range": (_I, [_I, _I, _I, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
@@ -234,6 +237,24 @@ def rtm_create_multi(nx, ny, nz, dx, dt, coeffs, devices):
     if not h:
         raise RtmError(RTM_EINVAL, _err())
     return h
+
+
+def rtm_create_batch(nx, ny, nz, dx, dt, coeffs, nshots):
+    c = _coeffs(coeffs)
+    h = lib.rtm_create_batch(int(nx), int(ny), int(nz), float(dx), float(dt), _ptr(c), int(nshots))
+    if not h:
+        raise RtmError(RTM_EINVAL if "CUDA" not in _err() else RTM_ECUDA, _err())
+    return h
+
+
+def rtm_num_shots(h) -> int:
+    return int(lib.rtm_num_shots(h))
+
+
+def rtm_inject_source_shot(h, shot, ix, iy, iz, samples):
+    s = _f32(samples)
+    return _check(lib.rtm_inject_source_shot(h, int(shot), int(ix), int(iy), int(iz),
+                                             _ptr(s) if s.size else None, int(s.size)))
 
 
 def rtm_get_unique_id() -> bytes:

@@ -410,3 +410,46 @@ def test_autotune_multislab(P):
         sim.step(4)
         got = sim.read_field()
     assert np.array_equal(got, gpu_run(P, v, 10.0, 1e-3, 4, u0=u0, up0=up0))
+
+
+# ----------------------------------------------------------------------------- batched shots (f3)
+@pytest.mark.parametrize("tile", [-1, 0, 5, 9])
+def test_batched_shots_equal_independent_runs(P, tile):
+    """A batch of shots on one velocity model = each shot run alone, bitwise; and each
+    matches the oracle.  Shots differ in ICs and sources (one shot has none)."""
+    nz, ny, nx = 23, 41, 68
+    rng = np.random.default_rng(3)
+    v = rng.uniform(1500, 4300, (nz, ny, nx)).astype(np.float32)
+    S = 3
+    ics = [ri.random_fields(v.shape, seed=200 + k) for k in range(S)]
+    w = ri.source_samples(3000.0, 1e-3, 15.0, 6)
+    srcs = {0: [(5, 6, 7, w)], 1: [], 2: [(60, 40, 22, -w), (0, 0, 0, 0.5 * w)]}
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, shots=S) as sim:
+        if tile != -1:
+            sim.set_tile(tile)
+        sim.set_velocity(v)
+        for k in range(S):
+            for s in srcs[k]:
+                sim.inject_source(*s, shot=k)
+        sim.set_fields(np.stack([a for a, _ in ics]), np.stack([b for _, b in ics]))
+        sim.step(6)
+        got = sim.read_field()
+        assert got.shape == (S, nz, ny, nx)
+    for k in range(S):
+        alone = gpu_run(P, v, 10.0, 1e-3, 6, u0=ics[k][0], up0=ics[k][1], sources=srcs[k],
+                        tile=tile)
+        assert np.array_equal(got[k], alone), k
+        orc = oracle.run(v, 10.0, 1e-3, C32, 6, u0=ics[k][0], up0=ics[k][1], sources=srcs[k])
+        assert relerr(got[k], orc) <= TOL_1 * 10
+
+
+def test_batch_errors(P):
+    with pytest.raises(P.RtmError):
+        P.rtm_create_batch(8, 8, 8, 10.0, 1e-3, C32, 0)
+    h = P.rtm_create_batch(8, 8, 8, 10.0, 1e-3, C32, 2)
+    try:
+        assert P.rtm_num_shots(h) == 2
+        with pytest.raises(P.RtmError):
+            P.rtm_inject_source_shot(h, 2, 1, 1, 1, np.ones(3, np.float32))
+    finally:
+        P.rtm_destroy(h)
