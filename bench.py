@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--tile", type=int, default=-1)
     ap.add_argument("--zchunk", type=int, default=0)
     ap.add_argument("--nsteps", type=int, default=0, help="override the config's time steps")
+    ap.add_argument("--shots", type=int, default=1,
+                    help="batched independent shots on the config's velocity model (f3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="short run for ncu captures (no extras)")
@@ -224,6 +226,9 @@ def main():
         tdist.broadcast_object_list(uid, src=0)
         h = P.rtm_create_dist(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32, rank, world,
                               uid[0], local)
+    elif args.shots > 1:
+        z0, nzl = 0, cfg.nz
+        h = P.rtm_create_batch(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32, args.shots)
     else:
         z0, nzl = 0, cfg.nz
         h = P.rtm_create(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32)
@@ -231,15 +236,18 @@ def main():
         P.rtm_set_tile(h, args.tile)
     if args.zchunk:
         P.rtm_set_zchunk(h, args.zchunk)
-    for (x, y, z, w) in cfg.sources(v_full):
-        P.rtm_inject_source(h, x, y, z, w[:nsteps] if len(w) > nsteps else w)
+    shots = max(1, args.shots) if world == 1 else 1
+    for k in range(shots):  # shot k: the config's sources moved along x (a shot line)
+        for (x, y, z, w) in cfg.sources(v_full):
+            xs = x if shots == 1 else (x + (k - shots // 2) * max(1, cfg.nx // (2 * shots))) % cfg.nx
+            P.rtm_inject_source_shot(h, k, xs, y, z, w[:nsteps] if len(w) > nsteps else w)
     stream = torch.cuda.Stream(device=dev)  # a real stream (the legacy default stream 0 cannot be adopted)
     P.rtm_set_stream(h, stream.cuda_stream)
     v_local = np.ascontiguousarray(v_full[z0:z0 + nzl])
     d_v = torch.from_numpy(v_local).to(dev)
-    d_out = torch.empty_like(d_v)
-    pts_local = cfg.nx * cfg.ny * nzl
-    pts_global = cfg.nx * cfg.ny * cfg.nz
+    d_out = torch.empty((shots,) + tuple(d_v.shape), dtype=torch.float32, device=dev)
+    pts_local = cfg.nx * cfg.ny * nzl * shots
+    pts_global = cfg.nx * cfg.ny * cfg.nz * shots
 
     def barrier():
         if world > 1:
@@ -299,9 +307,11 @@ def main():
     # roofline of the dominant kernel (the stencil): algorithmic 16 B/pt over its own
     # launch durations measured with CUDA events on the launching stream
     peak, peak_src = measured_peak()
-    alg_bytes = BYTES_PER_POINT * pts_local * nsteps * args.steps
+    # batched shots share C: 12 B/pt for u, u_prev, u_next + 4 B/pt of C per shot batch
+    bytes_per_pt = BYTES_PER_POINT if shots == 1 else 12.0 + 4.0 / shots
+    alg_bytes = bytes_per_pt * pts_local * nsteps * args.steps
     achieved = alg_bytes / (kms / 1e3) / 1e9 if kms > 0 else None
-    wl = f"C{cfg.k}"
+    wl = f"C{cfg.k}" if shots == 1 else f"C{cfg.k}x{shots}shots"
     traffic, traffic_src = ncu_traffic(wl, pts_local)
 
     # checksum of the result vs a plain host recomputation is in tests/; here a sanity read
@@ -311,7 +321,7 @@ def main():
     e2e = None
     if not args.no_e2e and not args.ncu:
         hv = torch.from_numpy(v_local).pin_memory()
-        hout = torch.empty(hv.shape, dtype=torch.float32).pin_memory()
+        hout = torch.empty(tuple(d_out.shape), dtype=torch.float32).pin_memory()
         hv_np, hout_np = hv.numpy(), hout.numpy()
 
         def e2e_step():
@@ -344,11 +354,12 @@ def main():
             "higher_is_better": True, "scaling": "strong" if cfg.k in (1, 2, 3, 4) else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, rtm_inputs)",
             "config": {"workload": wl, "grid": [cfg.nx, cfg.ny, cfg.nz], "time_steps": nsteps,
-                       "sources": len(cfg.sources_xyz), "parallelism": f"z-slab x{world}",
+                       "sources": len(cfg.sources_xyz), "shots": shots,
+                       "parallelism": f"z-slab x{world}",
                        "tile": tile_name, "l2": "inputs larger than L2 (3 x 4 GiB fields)"
                        if pts_local * 4 > 126e6 else "L2-resident (no flush)"},
-            "hbm_effective_gbs": round(value * BYTES_PER_POINT, 1),
-            "hbm_frac_of_8tbs": round(value * BYTES_PER_POINT / 8000.0, 4),
+            "hbm_effective_gbs": round(value * bytes_per_pt, 1),
+            "hbm_frac_of_8tbs": round(value * bytes_per_pt / 8000.0, 4),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
                          "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4) if achieved else None,
@@ -358,7 +369,8 @@ def main():
                                    + f"<{tile_name}>", "launches": kl,
                          "measured": roof_src,
                          "avg_launch_ms": round(kms / kl, 4) if kl else None,
-                         "alg_bytes_per_launch": BYTES_PER_POINT * pts_local * nsteps * args.steps // max(kl, 1),
+                         "alg_bytes_per_pt": bytes_per_pt,
+                         "alg_bytes_per_launch": int(alg_bytes // max(kl, 1)),
                          "traffic_source": traffic_src},
             "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks.summary(),
             "cpu_baseline": cpu, "finite": finite,

@@ -281,7 +281,7 @@ int finish_ctx(rtm_ctx* c) {
 int resolve_tile(const rtm_ctx* c) {
     if (c->nx % 4 != 0) return 0;  // 128-bit rows / TMA strides need nx % 4 == 0
     if (c->tile >= 0) return c->tile;
-    return 1;  // stream64x16k8d4: best/near-best on C3 and C4 (profiles/sweep_*_r01*.log)
+    return 13;  // stream64x16k8d4u11: best on C4 (profiles/sweep_c4_u1.log)
 }
 
 int encode_3d(CUtensorMap* tm, void* base, int nx, int ny, int nplanes, int bx, int by,

@@ -45,6 +45,7 @@ struct TileVariant {
     const char* name;
     int kind;                  // 0 naive, 1 k_tiled (CTA per unit), 2 k_stream (persistent, producer warp)
     int TX, TY, K, D, MINB;    // tile (x, y), u ring depth, u_prev/C ring depth (0: LDG), min CTAs/SM
+    int U;                     // z-loop unroll (register-queue rotation amortised over U planes)
 };
 
 // Variant table: index 0 is the naive kernel.

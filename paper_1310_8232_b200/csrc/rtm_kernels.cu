@@ -21,6 +21,7 @@
 #include "rtm_internal.h"
 
 #include <cstdio>
+#include <type_traits>
 
 namespace rtm {
 
@@ -380,6 +381,33 @@ __global__ void __launch_bounds__(256) k_velocity(const float* v, float* C, long
 // unit boundaries.  Work units are (z-chunk, tile) pairs, chunk-major, dealt round-robin
 // to the persistent CTAs (unit = blockIdx.x + k * gridDim.x) so co-running CTAs are xy
 // neighbours at similar z.
+__device__ __forceinline__ void mbar_wait_u32(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(addr), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t addr) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+// Run f(integral_constant<O>), f(<O+1>), ... f(<U-1>) while iterations remain; false when the
+// unit ended inside the unrolled group.
+template <int O, int U, class F>
+__device__ __forceinline__ bool unrolled(F& f, int i, int n) {
+    f(std::integral_constant<int, O>{});
+    if constexpr (O + 1 < U) {
+        if (i + O + 1 >= n) return false;
+        return unrolled<O + 1, U>(f, i, n);
+    }
+    return true;
+}
+
 template <int TX, int TY, int K, int D>
 struct StreamShape {
     static constexpr int NW = TX * TY / 128;      // consumer warps (4 points per thread)
@@ -463,7 +491,7 @@ __device__ __forceinline__ UnitGeom unit_geom(const StencilParams& p, int unit, 
     return g;
 }
 
-template <int TX, int TY, int K, int D, int MINB>
+template <int TX, int TY, int K, int D, int MINB, int U>
 __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
     k_stream(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_up,
              const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ StencilParams p) {
@@ -543,11 +571,10 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
     const int pf_mode = p.cache_mode & 3;
     const int pf_dist = (p.cache_mode >> 4) & 15;
     const bool plain = (p.cache_mode & 8) != 0;
+    const uint32_t fu = smem_u32(full_u), eu = smem_u32(empty_u);
+    const uint32_t fc = smem_u32(full_c), ec = smem_u32(empty_c);
+    const float* uown = uring + own;
     uint32_t gu = 0, gc = 0;
-    auto release_u = [&](uint32_t seq) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_u[seq % K]);
-    };
     for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
         const UnitGeom g = unit_geom(p, unit, TX, TY);
         const int n = g.ze - g.zs;
@@ -566,14 +593,22 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
         float* outp = p.next + (g.soff + g.zs + 5) * p.plane + col;  // also u_prev (D == 0)
         const float* cp = p.C + (long long)g.zs * p.plane + col;
 
-        float4 q[11];
+        // register queue along z: q[O + k] = u(z - 5 + k) for the O-th unrolled iteration
+        float4 q[10 + U];
 #pragma unroll
         for (int j = 0; j < 10; ++j) {
             const uint32_t seq = gu + j;
-            mbar_wait(&full_u[seq % K], (seq / K) & 1);
-            q[j] = *reinterpret_cast<const float4*>(uring + (seq % K) * S::USLOT + own);
-            if (j < 5) release_u(seq);
+            mbar_wait_u32(fu + 8 * (seq % K), (seq / K) & 1);
+            q[j] = *reinterpret_cast<const float4*>(uown + (seq % K) * S::USLOT);
+            if (j < 5) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive_u32(eu + 8 * (seq % K));
+            }
         }
+        // running ring positions: plane gu+i+10 (new), gu+i+5 (current), u_prev/C gc+i
+        uint32_t sn = (gu + 10) % K, pn = ((gu + 10) / K) & 1;
+        uint32_t sc = (gu + 5) % K;
+        uint32_t sq = D > 0 ? gc % D : 0, pq = D > 0 ? (gc / D) & 1 : 0;
         float4 upv = make_float4(0.f, 0.f, 0.f, 0.f), cv = upv;
         if constexpr (D == 0) {
             if (active) {
@@ -581,37 +616,36 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
                 cv = ld_mode4(cp, plain);
             }
         }
-#pragma unroll 1
-        for (int i = 0; i < n; ++i) {
+        int it = 0;
+        auto body = [&](auto OFF) {
+            constexpr int O = decltype(OFF)::value;
             float4 upn = upv, cn = cv;
             if constexpr (D == 0) {
-                if (active && i + 1 < n) {
+                if (active && it + 1 < n) {
                     upn = ld_mode4(outp + p.plane, plain);
                     cn = ld_mode4(cp + p.plane, plain);
-                    if (pf_mode && i + pf_dist < n) {
+                    if (pf_mode && it + pf_dist < n) {
                         prefetch_l2(outp + pf_dist * p.plane, pf_mode);
                         prefetch_l2(cp + pf_dist * p.plane, pf_mode);
                     }
                 }
             }
-            const uint32_t sn = gu + i + 10, sc = gu + i + 5;
-            mbar_wait(&full_u[sn % K], (sn / K) & 1);
-            q[10] = *reinterpret_cast<const float4*>(uring + (sn % K) * S::USLOT + own);
+            mbar_wait_u32(fu + 8 * sn, pn);
+            q[O + 10] = *reinterpret_cast<const float4*>(uown + sn * S::USLOT);
             if constexpr (D > 0) {
-                const uint32_t cs = gc + i;
-                mbar_wait(&full_c[cs % D], (cs / D) & 1);
-                const float* cb = cring + (cs % D) * S::CSLOT + cown;
+                mbar_wait_u32(fc + 8 * sq, pq);
+                const float* cb = cring + sq * S::CSLOT + cown;
                 upv = *reinterpret_cast<const float4*>(cb);
                 cv = *reinterpret_cast<const float4*>(cb + TX * TY);
             }
-            const float* row = uring + (sc % K) * S::USLOT + own;
+            const float* row = uown + sc * S::USLOT;
             float xs[14];
             {
                 const float4 l = *reinterpret_cast<const float4*>(row - 4);
                 const float4 rr = *reinterpret_cast<const float4*>(row + 4);
                 xs[0] = row[-5];
                 xs[1] = l.x; xs[2] = l.y; xs[3] = l.z; xs[4] = l.w;
-                xs[5] = q[5].x; xs[6] = q[5].y; xs[7] = q[5].z; xs[8] = q[5].w;
+                xs[5] = q[O + 5].x; xs[6] = q[O + 5].y; xs[7] = q[O + 5].z; xs[8] = q[O + 5].w;
                 xs[9] = rr.x; xs[10] = rr.y; xs[11] = rr.z; xs[12] = rr.w;
                 xs[13] = row[8];
             }
@@ -621,34 +655,49 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
                 yv[5 - m] = *reinterpret_cast<const float4*>(row - m * S::RS);
                 yv[5 + m] = *reinterpret_cast<const float4*>(row + m * S::RS);
             }
-            yv[5] = q[5];
+            yv[5] = q[O + 5];
             float out[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 float zl[11], yl[11], xl[11];
 #pragma unroll
                 for (int o = 0; o < 11; ++o) {
-                    zl[o] = comp(q[o], k);
+                    zl[o] = comp(q[O + o], k);
                     yl[o] = comp(yv[o], k);
                     xl[o] = xs[k + o];
                 }
                 out[k] = rtm_point(zl, yl, xl, comp(upv, k), comp(cv, k), c);
             }
-            release_u(sc);
-            if constexpr (D > 0) {
-                if (lane == 0) mbar_arrive(&empty_c[(gc + i) % D]);  // after the same __syncwarp
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive_u32(eu + 8 * sc);
+                if constexpr (D > 0) mbar_arrive_u32(ec + 8 * sq);
             }
-            if (smask) add_sources(p, smask, x, g.zs + i, out);
+            if (smask) add_sources(p, smask, x, g.zs + it, out);
             if (active) st_mode4(outp, make_float4(out[0], out[1], out[2], out[3]), plain);
-#pragma unroll
-            for (int o = 0; o < 10; ++o) q[o] = q[o + 1];
-            upv = upn;
-            cv = cn;
+            if (++sn == K) sn = 0, pn ^= 1;
+            if (++sc == K) sc = 0;
+            if constexpr (D > 0) {
+                if (++sq == D) sq = 0, pq ^= 1;
+            } else {
+                upv = upn;
+                cv = cn;
+            }
             outp += p.plane;
             cp += p.plane;
+            ++it;
+        };
+#pragma unroll 1
+        for (int i = 0; i < n; i += U) {
+            if (!unrolled<0, U>(body, i, n)) break;
+#pragma unroll
+            for (int o = 0; o < 10; ++o) q[o] = q[o + U];
         }
 #pragma unroll 1
-        for (int j = n + 5; j < n + 10; ++j) release_u(gu + j);  // planes used only by the queue
+        for (int j = n + 5; j < n + 10; ++j) {  // planes used only by the queue
+            __syncwarp();
+            if (lane == 0) mbar_arrive_u32(eu + 8 * ((gu + j) % K));
+        }
         gu += n + 10;
         gc += n;
     }
@@ -656,24 +705,26 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
 
 // ------------------------------------------------------------------------------------
 // Variant table.  id 0 = naive; kind 1 = k_tiled; kind 2 = k_stream.
-#define RTM_VARIANTS(X)                               \
-    X(1, "stream64x16k8d4", 2, 64, 16, 8, 4, 2)       \
-    X(2, "stream64x16k9d0", 2, 64, 16, 9, 0, 2)       \
-    X(3, "stream64x32k8d3", 2, 64, 32, 8, 3, 1)       \
-    X(4, "stream128x16k8d3", 2, 128, 16, 8, 3, 1)     \
-    X(5, "stream32x32k8d4", 2, 32, 32, 8, 4, 2)       \
-    X(6, "stream64x8k8d4", 2, 64, 8, 8, 4, 3)         \
-    X(7, "stream128x8k8d4", 2, 128, 8, 8, 4, 2)       \
-    X(8, "stream64x32k10d0", 2, 64, 32, 10, 0, 1)     \
-    X(9, "tma64x16k10", 1, 64, 16, 10, 0, 2)          \
-    X(10, "tma32x16k10", 1, 32, 16, 10, 0, 3)         \
-    X(11, "tma64x8k10", 1, 64, 8, 10, 0, 3)           \
-    X(12, "tma128x8k10", 1, 128, 8, 10, 0, 2)         \
-    X(13, "tma32x32k10", 1, 32, 32, 10, 0, 2)
+#define RTM_VARIANTS(X)                                  \
+    X(1, "stream64x16k8d4u4", 2, 64, 16, 8, 4, 2, 4)     \
+    X(2, "stream64x16k8d4", 2, 64, 16, 8, 4, 2, 1)       \
+    X(3, "stream64x16k8d4u2", 2, 64, 16, 8, 4, 2, 2)     \
+    X(4, "stream32x32k8d4u4", 2, 32, 32, 8, 4, 2, 4)     \
+    X(5, "stream64x16k9d0u4", 2, 64, 16, 9, 0, 2, 4)     \
+    X(6, "stream64x32k10d0u4", 2, 64, 32, 10, 0, 1, 4)   \
+    X(7, "stream64x14k8d4u2", 2, 64, 14, 8, 4, 2, 2)     \
+    X(8, "stream64x14k8d4u4", 2, 64, 14, 8, 4, 2, 4)     \
+    X(9, "stream128x7k8d4u2", 2, 128, 7, 8, 4, 2, 2)     \
+    X(10, "stream128x7k8d4u4", 2, 128, 7, 8, 4, 2, 4)    \
+    X(11, "stream64x14k8d4u11", 2, 64, 14, 8, 4, 2, 11)  \
+    X(12, "stream32x28k8d4u4", 2, 32, 28, 8, 4, 2, 4)    \
+    X(13, "stream64x16k8d4u11", 2, 64, 16, 8, 4, 2, 11)  \
+    X(14, "tma64x16k10", 1, 64, 16, 10, 0, 2, 1)         \
+    X(15, "tma32x16k10", 1, 32, 16, 10, 0, 3, 1)
 
 static const TileVariant kVariants[] = {
-    {"naive", 0, 0, 0, 0, 0, 0},
-#define X(id, name, kind, tx, ty, k, d, mb) {name, kind, tx, ty, k, d, mb},
+    {"naive", 0, 0, 0, 0, 0, 0, 1},
+#define X(id, name, kind, tx, ty, k, d, mb, u) {name, kind, tx, ty, k, d, mb, u},
     RTM_VARIANTS(X)
 #undef X
 };
@@ -681,7 +732,7 @@ static const TileVariant kVariants[] = {
 int num_variants() { return static_cast<int>(sizeof(kVariants) / sizeof(kVariants[0])); }
 const TileVariant& variant(int id) { return kVariants[id]; }
 
-template <int KIND, int TX, int TY, int K, int D, int MINB>
+template <int KIND, int TX, int TY, int K, int D, int MINB, int U>
 static cudaError_t prepare(const void** fn, int* threads, size_t* smem) {
     if constexpr (KIND == 1) {
         using S = TiledShape<TX, TY, K>;
@@ -690,7 +741,7 @@ static cudaError_t prepare(const void** fn, int* threads, size_t* smem) {
         *smem = S::SMEM;
     } else {
         using S = StreamShape<TX, TY, K, D>;
-        *fn = reinterpret_cast<const void*>(&k_stream<TX, TY, K, D, MINB>);
+        *fn = reinterpret_cast<const void*>(&k_stream<TX, TY, K, D, MINB, U>);
         *threads = S::NT;
         *smem = S::SMEM;
     }
@@ -700,9 +751,9 @@ static cudaError_t prepare(const void** fn, int* threads, size_t* smem) {
 
 static cudaError_t variant_fn(int id, const void** fn, int* threads, size_t* smem) {
     switch (id) {
-#define X(vid, name, kind, tx, ty, k, d, mb) \
-    case vid:                                \
-        return prepare<kind, tx, ty, k, d, mb>(fn, threads, smem);
+#define X(vid, name, kind, tx, ty, k, d, mb, u) \
+    case vid:                                   \
+        return prepare<kind, tx, ty, k, d, mb, u>(fn, threads, smem);
         RTM_VARIANTS(X)
 #undef X
         default:

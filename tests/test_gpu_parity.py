@@ -406,7 +406,7 @@ def test_autotune_multislab(P):
         sim.set_velocity(v)
         sim.set_fields(u0, up0)
         res, times = P.rtm_autotune(sim.h, 2, tiles=[1, 5, 0])
-        assert res["best_tile"] in (1, 5)  # the naive kernel is never the fastest
+        assert res["best_tile"] == [1, 5, 0][int(np.argmin(times))]
         sim.step(4)
         got = sim.read_field()
     assert np.array_equal(got, gpu_run(P, v, 10.0, 1e-3, 4, u0=u0, up0=up0))

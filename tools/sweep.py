@@ -21,13 +21,17 @@ def main():
     ap.add_argument("--zchunk", default="0")
     ap.add_argument("--cache", default="", help="comma list of RTM_OPT_CACHE_MODE values (hex ok)")
     ap.add_argument("--repeat", type=int, default=1, help="interleaved repetitions (min is kept)")
+    ap.add_argument("--shots", type=int, default=1)
     args = ap.parse_args()
     import torch
     import paper_1310_8232_b200 as P
     import rtm_inputs as ri
     cfg = ri.make_config(args.config)
     v = cfg.velocity()
-    h = P.rtm_create(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32)
+    if args.shots > 1:
+        h = P.rtm_create_batch(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32, args.shots)
+    else:
+        h = P.rtm_create(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32)
     P.rtm_set_velocity(h, v)
     for s in cfg.sources(v):
         P.rtm_inject_source(h, *s)
@@ -50,7 +54,7 @@ def main():
             e1.record(st)
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / args.ni
-            gpts = cfg.points / ms / 1e6
+            gpts = cfg.points * args.shots / ms / 1e6
             r = {"tile": t, "name": P.rtm_tile_name(t), "zchunk": zc,
                  "cache": hex(P.rtm_get_option(h, P.RTM_OPT_CACHE_MODE)), "ms_per_step": round(ms, 4),
                  "gpts": round(gpts, 2), "eff_gbs": round(16 * gpts, 1)}
