@@ -39,7 +39,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--tile", type=int, default=-1)
+    ap.add_argument("--tile", type=int, default=-1,
+                    help="kernel variant; -1 = choose with rtm_autotune (untimed, before warm-up)")
+    ap.add_argument("--tune-ni", type=int, default=4, help="autotune iterations per candidate")
     ap.add_argument("--zchunk", type=int, default=0)
     ap.add_argument("--nsteps", type=int, default=0, help="override the config's time steps")
     ap.add_argument("--shots", type=int, default=1,
@@ -248,6 +250,17 @@ def main():
     d_out = torch.empty((shots,) + tuple(d_v.shape), dtype=torch.float32, device=dev)
     pts_local = cfg.nx * cfg.ny * nzl * shots
     pts_global = cfg.nx * cfg.ny * cfg.nz * shots
+    tune = None
+    if args.tile == -1 and not args.ncu:
+        # the paper's two-phase blocksize selection, GPU analogue: every
+        # stream-kernel variant timed on this grid (max over ranks = MWMB), winner verified
+        P.rtm_set_velocity_device(h, d_v.data_ptr())
+        cands = [t for t in range(P.rtm_num_tiles()) if (P.rtm_tile_name(t) or "").startswith("stream")]
+        res, times = P.rtm_autotune(h, args.tune_ni, tiles=cands)
+        tune = {"selected": P.rtm_tile_name(res["best_tile"]), "candidates": len(cands),
+                "nI": args.tune_ni, "min_time_ms": round(res["min_time_ms"], 4),
+                "actual_time_ms": round(res["actual_time_ms"], 4),
+                "quality_pct": round(res["quality_pct"], 2)}
 
     def barrier():
         if world > 1:
@@ -373,6 +386,7 @@ def main():
                          "alg_bytes_per_launch": int(alg_bytes // max(kl, 1)),
                          "traffic_source": traffic_src},
             "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks.summary(),
+            "autotune": tune,
             "cpu_baseline": cpu, "finite": finite,
         }
         print(json.dumps(line), flush=True)

@@ -122,8 +122,10 @@ const char* rtm_tile_name(int tile_id);  /* e.g. "stream64x32k10d0"; NULL for un
  *                      accesses, bits 4-7 prefetch distance in planes, bits 8-9 L2 promotion
  *                      of the halo'd u TMA box (0 = 256B, 1 = 128B, 2 = 64B, 3 = none)
  *   RTM_OPT_GRAPHS     1 (default) = capture runs of 16 steps in CUDA graphs, 0 = direct launches
+ *   RTM_OPT_SHOT_ORDER batched contexts: 0 auto (shot-major when C fits in 40% of L2), 1 shot-major
+ *                      (each shot's tiles co-run), 2 shot-fastest (co-running CTAs share C tiles)
  * Unknown key or out-of-range value -> RTM_EINVAL.  rtm_get_option returns -1 for unknown keys. */
-enum { RTM_OPT_ZCHUNK = 1, RTM_OPT_CACHE_MODE = 2, RTM_OPT_GRAPHS = 3 };
+enum { RTM_OPT_ZCHUNK = 1, RTM_OPT_CACHE_MODE = 2, RTM_OPT_GRAPHS = 3, RTM_OPT_SHOT_ORDER = 4 };
 int rtm_set_option(rtm_ctx* ctx, int key, long long value);
 long long rtm_get_option(rtm_ctx* ctx, int key);
 

@@ -117,6 +117,8 @@ struct rtm_ctx {
     int tile = -1;
     int zchunk = 0;  // 0 = auto
     int cache_mode = 0x41;  // L2 prefetch of u_prev/C 4 planes ahead, evict_last (tuned)
+    int shot_order = 0;     // 0 auto, 1 shot-major, 2 shot-fastest
+    int l2_bytes = 0;
     bool graphs = true;
     std::vector<HostSource> sources;
     bool profiling = false;
@@ -274,6 +276,7 @@ int finish_ctx(rtm_ctx* c) {
     CK(cudaEventCreate(&c->t0));
     CK(cudaEventCreate(&c->t1));
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->slabs[0].dev));
+    CK(cudaDeviceGetAttribute(&c->l2_bytes, cudaDevAttrL2CacheSize, c->slabs[0].dev));
     for (auto& s : c->slabs) RET(alloc_slab(c, s));
     return RTM_OK;
 }
@@ -361,6 +364,11 @@ void fill_params(const rtm_ctx* c, const Slab& s, int parity, StencilParams& p) 
     for (int k = 0; k < p.nsrc; ++k) p.src[k] = s.srcs[k];
     p.samples = s.d_samples;
     p.cache_mode = c->cache_mode;
+    // auto: shot-major when one C field fits comfortably in L2 (it is then re-read from L2 by
+    // every shot and the shots keep the full co-running tile set for halo reuse); otherwise
+    // shot-fastest so co-running CTAs share each C tile
+    const double c_bytes = 4.0 * c->nx * c->ny * s.nzl;
+    p.shot_major = c->shot_order == 1 ? 1 : c->shot_order == 2 ? 0 : (c_bytes <= 0.4 * c->l2_bytes ? 1 : 0);
 }
 
 // Launch the stencil on planes [b0,b0+l0) (+ [b1,b1+l1) if l1 > 0) of slab s.
@@ -1049,6 +1057,10 @@ int rtm_set_option(rtm_ctx* c, int key, long long value) {
         case RTM_OPT_GRAPHS:
             c->graphs = value != 0;
             break;
+        case RTM_OPT_SHOT_ORDER:
+            if (value < 0 || value > 2) return fail(RTM_EINVAL, "shot order %lld not in 0..2", value);
+            c->shot_order = (int)value;
+            break;
         default:
             return fail(RTM_EINVAL, "unknown option key %d", key);
     }
@@ -1062,6 +1074,7 @@ long long rtm_get_option(rtm_ctx* c, int key) {
         case RTM_OPT_ZCHUNK: return c->zchunk;
         case RTM_OPT_CACHE_MODE: return c->cache_mode;
         case RTM_OPT_GRAPHS: return c->graphs ? 1 : 0;
+        case RTM_OPT_SHOT_ORDER: return c->shot_order;
         default: return -1;
     }
 }

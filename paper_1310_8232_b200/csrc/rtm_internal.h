@@ -36,6 +36,8 @@ struct StencilParams {
     int r_chunks[2];           // z-chunks per range (tiled kernel work units)
     int tiles_x, tiles_y;      // tiled kernel: xy tiles
     int cache_mode;            // k_stream L2 policy knobs (see rtm_kernels.cu)
+    int shot_major;            // 1: units ordered shot-slowest (each shot's tiles co-run);
+                               // 0: shot-fastest (co-running CTAs share the C tile)
     int nsrc;
     DevSource src[RTM_MAX_SOURCES];
     const float* samples;

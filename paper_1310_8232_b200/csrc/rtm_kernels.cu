@@ -43,6 +43,28 @@ __device__ __forceinline__ float rtm_point(const float (&z)[11], const float (&y
     return __fmaf_rn(C, acc, __fmaf_rn(2.0f, z[5], -up));
 }
 
+// The same expression for two x-adjacent points at once with Blackwell's packed fp32x2
+// instructions (FFMA2/FADD2/FMUL2: one issue slot for two lanes).  Each lane performs exactly
+// rtm_point's IEEE operations in rtm_point's order, so results are bitwise identical.  The x
+// pair sums c_m * (x[-m] + x[+m]) are passed in precomputed (xsum[m-1]).
+__device__ __forceinline__ float2 rtm_point2(const float2 (&z)[11], const float2 (&y)[11],
+                                             const float2 (&xsum)[5], float2 up, float2 C,
+                                             const float (&c)[6]) {
+    float2 acc = __fmul2_rn(make_float2(c[0], c[0]), z[5]);
+#pragma unroll
+    for (int m = 1; m <= 5; ++m)
+        acc = __ffma2_rn(make_float2(c[m], c[m]), __fadd2_rn(z[5 - m], z[5 + m]), acc);
+#pragma unroll
+    for (int m = 1; m <= 5; ++m)
+        acc = __ffma2_rn(make_float2(c[m], c[m]), __fadd2_rn(y[5 - m], y[5 + m]), acc);
+#pragma unroll
+    for (int m = 1; m <= 5; ++m) acc = __ffma2_rn(make_float2(c[m], c[m]), xsum[m - 1], acc);
+    const float2 lf = __ffma2_rn(make_float2(2.0f, 2.0f), z[5], make_float2(-up.x, -up.y));
+    return __ffma2_rn(C, acc, lf);
+}
+__device__ __forceinline__ float2 lo2(const float4& v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(const float4& v) { return make_float2(v.z, v.w); }
+
 // ------------------------------------------------------------------------------------
 // PTX helpers: mbarrier + TMA
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -144,8 +166,9 @@ __global__ void __launch_bounds__(TX * TY / 4, MINB)
 
     // ---- work unit: (z-chunk, tile), chunk-major so concurrently running CTAs are xy
     // neighbours at similar z (their halo re-reads hit L2)
-    const int shot = blockIdx.x % p.nshots;
-    const int ublk = blockIdx.x / p.nshots;
+    const int nunits_shot = p.tiles_x * p.tiles_y * (p.r_chunks[0] + (p.nranges > 1 ? p.r_chunks[1] : 0));
+    const int shot = p.shot_major ? (int)(blockIdx.x / nunits_shot) : (int)(blockIdx.x % p.nshots);
+    const int ublk = p.shot_major ? (int)(blockIdx.x - shot * nunits_shot) : (int)(blockIdx.x / p.nshots);
     const long long soff = (long long)shot * (p.nzl + 10);
     const int ntiles = p.tiles_x * p.tiles_y;
     int chunk = ublk / ntiles;
@@ -470,9 +493,16 @@ struct UnitGeom {
 // unit = ((chunk * ntiles) + tile) * nshots + shot: shots fastest (concurrent CTAs share the
 // C tile through L2), then tiles (co-running xy neighbours share halos), then z-chunks.
 __device__ __forceinline__ UnitGeom unit_geom(const StencilParams& p, int unit, int TX, int TY) {
-    const int shot = unit % p.nshots;
-    unit /= p.nshots;
     const int ntiles = p.tiles_x * p.tiles_y;
+    int shot;
+    if (p.shot_major) {
+        const int per_shot = ntiles * (p.r_chunks[0] + (p.nranges > 1 ? p.r_chunks[1] : 0));
+        shot = unit / per_shot;
+        unit -= shot * per_shot;
+    } else {
+        shot = unit % p.nshots;
+        unit /= p.nshots;
+    }
     int chunk = unit / ntiles;
     const int tile = unit - chunk * ntiles;
     int r = 0;
@@ -657,16 +687,33 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
             }
             yv[5] = q[O + 5];
             float out[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                float zl[11], yl[11], xl[11];
+            {
+                // x pair sums for points (0,1) and (2,3): even m are aligned register pairs
+                // of the staged float4s (FADD2), odd m straddle them (two scalar FADDs)
+                const float4 L4 = make_float4(xs[1], xs[2], xs[3], xs[4]);
+                const float4 R4 = make_float4(xs[9], xs[10], xs[11], xs[12]);
+                float2 xa[5], xb[5];
+                xa[0] = make_float2(__fadd_rn(xs[4], xs[6]), __fadd_rn(xs[5], xs[7]));
+                xa[1] = __fadd2_rn(hi2(L4), hi2(q[O + 5]));
+                xa[2] = make_float2(__fadd_rn(xs[2], xs[8]), __fadd_rn(xs[3], xs[9]));
+                xa[3] = __fadd2_rn(lo2(L4), lo2(R4));
+                xa[4] = make_float2(__fadd_rn(xs[0], xs[10]), __fadd_rn(xs[1], xs[11]));
+                xb[0] = make_float2(__fadd_rn(xs[6], xs[8]), __fadd_rn(xs[7], xs[9]));
+                xb[1] = __fadd2_rn(lo2(q[O + 5]), lo2(R4));
+                xb[2] = make_float2(__fadd_rn(xs[4], xs[10]), __fadd_rn(xs[5], xs[11]));
+                xb[3] = __fadd2_rn(hi2(L4), hi2(R4));
+                xb[4] = make_float2(__fadd_rn(xs[2], xs[12]), __fadd_rn(xs[3], xs[13]));
+                float2 za[11], zb[11], ya[11], yb[11];
 #pragma unroll
                 for (int o = 0; o < 11; ++o) {
-                    zl[o] = comp(q[O + o], k);
-                    yl[o] = comp(yv[o], k);
-                    xl[o] = xs[k + o];
+                    za[o] = lo2(q[O + o]);
+                    zb[o] = hi2(q[O + o]);
+                    ya[o] = lo2(yv[o]);
+                    yb[o] = hi2(yv[o]);
                 }
-                out[k] = rtm_point(zl, yl, xl, comp(upv, k), comp(cv, k), c);
+                const float2 ra = rtm_point2(za, ya, xa, lo2(upv), lo2(cv), c);
+                const float2 rb = rtm_point2(zb, yb, xb, hi2(upv), hi2(cv), c);
+                out[0] = ra.x; out[1] = ra.y; out[2] = rb.x; out[3] = rb.y;
             }
             __syncwarp();
             if (lane == 0) {
@@ -720,7 +767,18 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
     X(12, "stream32x28k8d4u4", 2, 32, 28, 8, 4, 2, 4)    \
     X(13, "stream64x16k8d4u11", 2, 64, 16, 8, 4, 2, 11)  \
     X(14, "tma64x16k10", 1, 64, 16, 10, 0, 2, 1)         \
-    X(15, "tma32x16k10", 1, 32, 16, 10, 0, 3, 1)
+    X(15, "tma32x16k10", 1, 32, 16, 10, 0, 3, 1)         \
+    X(16, "stream64x14k10d4u4", 2, 64, 14, 10, 4, 2, 4)  \
+    X(17, "stream64x14k10d5u4", 2, 64, 14, 10, 5, 2, 4)  \
+    X(18, "stream64x16k9d4u11", 2, 64, 16, 9, 4, 2, 11)  \
+    X(19, "stream128x7k9d3u4", 2, 128, 7, 9, 3, 2, 4)    \
+    X(20, "stream64x14k10d4u11", 2, 64, 14, 10, 4, 2, 11) \
+    X(21, "stream64x14k12d3u4", 2, 64, 14, 12, 3, 2, 4)  \
+    X(22, "stream64x16k8d5u11", 2, 64, 16, 8, 5, 2, 11)  \
+    X(23, "stream64x14k9d6u4", 2, 64, 14, 9, 6, 2, 4)    \
+    X(24, "stream64x14k8d7u4", 2, 64, 14, 8, 7, 2, 4)    \
+    X(25, "stream32x28k10d5u4", 2, 32, 28, 10, 5, 2, 4)  \
+    X(26, "stream64x14k10d5u11", 2, 64, 14, 10, 5, 2, 11)
 
 static const TileVariant kVariants[] = {
     {"naive", 0, 0, 0, 0, 0, 0, 1},

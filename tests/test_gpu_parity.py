@@ -413,8 +413,8 @@ def test_autotune_multislab(P):
 
 
 # ----------------------------------------------------------------------------- batched shots (f3)
-@pytest.mark.parametrize("tile", [-1, 0, 5, 9])
-def test_batched_shots_equal_independent_runs(P, tile):
+@pytest.mark.parametrize("tile,order", [(-1, 0), (0, 0), (5, 1), (9, 2), (-1, 1), (-1, 2), (14, 1), (14, 2)])
+def test_batched_shots_equal_independent_runs(P, tile, order):
     """A batch of shots on one velocity model = each shot run alone, bitwise; and each
     matches the oracle.  Shots differ in ICs and sources (one shot has none)."""
     nz, ny, nx = 23, 41, 68
@@ -427,6 +427,7 @@ def test_batched_shots_equal_independent_runs(P, tile):
     with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, shots=S) as sim:
         if tile != -1:
             sim.set_tile(tile)
+        P.rtm_set_option(sim.h, P.RTM_OPT_SHOT_ORDER, order)
         sim.set_velocity(v)
         for k in range(S):
             for s in srcs[k]:

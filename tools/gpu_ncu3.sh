@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+B="python tools/sweep.py --config 2 --ni 2 --shots 16 --tiles 10"
+$B > gpurun_out/n3b_plain.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_stream -s 4 -c 1 -o gpurun_out/prof_c2s16_x2 $B > gpurun_out/n3b.log 2>&1
+A="python tools/sweep.py --config 4 --ni 2 --tiles 13"
+$A > gpurun_out/n3a_plain.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_stream -s 4 -c 1 -o gpurun_out/prof_c4_x2 $A > gpurun_out/n3a.log 2>&1
+echo done

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--cache", default="", help="comma list of RTM_OPT_CACHE_MODE values (hex ok)")
     ap.add_argument("--repeat", type=int, default=1, help="interleaved repetitions (min is kept)")
     ap.add_argument("--shots", type=int, default=1)
+    ap.add_argument("--shot-order", default="0", help="comma list of RTM_OPT_SHOT_ORDER values")
     args = ap.parse_args()
     import torch
     import paper_1310_8232_b200 as P
@@ -40,8 +41,10 @@ def main():
     tiles = [int(t) for t in args.tiles.split(",")] if args.tiles else list(range(P.rtm_num_tiles()))
     res = []
     for t in [t for _ in range(args.repeat) for t in tiles]:
-        for zc, cm in [(int(z), c) for z in args.zchunk.split(",")
-                       for c in ([int(x, 0) for x in args.cache.split(",")] if args.cache else [None])]:
+        for zc, cm, so in [(int(z), c, int(o)) for z in args.zchunk.split(",")
+                           for c in ([int(x, 0) for x in args.cache.split(",")] if args.cache else [None])
+                           for o in args.shot_order.split(",")]:
+            P.rtm_set_option(h, P.RTM_OPT_SHOT_ORDER, so)
             P.rtm_set_tile(h, t)
             P.rtm_set_zchunk(h, zc)
             if cm is not None:
@@ -55,14 +58,14 @@ def main():
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / args.ni
             gpts = cfg.points * args.shots / ms / 1e6
-            r = {"tile": t, "name": P.rtm_tile_name(t), "zchunk": zc,
+            r = {"tile": t, "name": P.rtm_tile_name(t), "zchunk": zc, "shot_order": so,
                  "cache": hex(P.rtm_get_option(h, P.RTM_OPT_CACHE_MODE)), "ms_per_step": round(ms, 4),
                  "gpts": round(gpts, 2), "eff_gbs": round(16 * gpts, 1)}
             res.append(r)
             print(json.dumps(r), flush=True)
     agg = {}
     for r in res:
-        k = (r["tile"], r["zchunk"], r["cache"])
+        k = (r["tile"], r["zchunk"], r["cache"], r["shot_order"])
         if k not in agg or r["ms_per_step"] < agg[k]["ms_per_step"]:
             agg[k] = r
     for r in sorted(agg.values(), key=lambda r: r["ms_per_step"]):
