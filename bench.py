@@ -67,13 +67,15 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(cfg_name, nsteps_per_launch_pts):
+def ncu_traffic(cfg_name, tile_name):
     """dram read+write bytes per launch of the dominant kernel from the committed ncu
-    --set full summary (profiles/), if one exists for this workload."""
+    --set full summary (profiles/ncu_full_<workload>_<round>.json) for this workload and
+    kernel variant, if one exists."""
     for p in sorted((ROOT / "profiles").glob("ncu_full_*.json"), reverse=True):
         try:
             d = json.loads(p.read_text())
-            if d.get("workload") == cfg_name and d.get("dram_bytes_per_launch"):
+            if (d.get("workload") == cfg_name and d.get("tile") == tile_name
+                    and d.get("dram_bytes_per_launch")):
                 return float(d["dram_bytes_per_launch"]), p.name
         except Exception:
             continue
@@ -325,7 +327,7 @@ def main():
     alg_bytes = bytes_per_pt * pts_local * nsteps * args.steps
     achieved = alg_bytes / (kms / 1e3) / 1e9 if kms > 0 else None
     wl = f"C{cfg.k}" if shots == 1 else f"C{cfg.k}x{shots}shots"
-    traffic, traffic_src = ncu_traffic(wl, pts_local)
+    traffic, traffic_src = ncu_traffic(wl, P.rtm_tile_name(P.rtm_get_tile(h)))
 
     # checksum of the result vs a plain host recomputation is in tests/; here a sanity read
     finite = bool(torch.isfinite(d_out).all().item())

@@ -8,7 +8,15 @@ timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/p
 timeout 600 python bench.py > gpurun_out/bench_$TAG.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_$TAG.log
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_$TAG.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref_$TAG.log
 for c in 3 5 2 1; do timeout 600 python bench.py --config $c --no-cpu > gpurun_out/bench_c${c}_$TAG.log 2>&1; done
-B="python bench.py --ncu --steps 1 --warmup 0 --nsteps 3"
+# profile the variant the bench's autotune selected on this box
+TILE=$(python -c "
+import json,sys
+import paper_1310_8232_b200 as P
+d=[json.loads(l) for l in open('gpurun_out/bench_$TAG.log') if l.startswith('{')][0]
+name=(d.get('autotune') or {}).get('selected') or d['config']['tile']
+print([i for i in range(P.rtm_num_tiles()) if P.rtm_tile_name(i)==name][0])" 2>/dev/null || echo -1)
+echo "ncu tile $TILE" > gpurun_out/ncu_tile_$TAG.txt
+B="python bench.py --ncu --steps 1 --warmup 0 --nsteps 3 --tile $TILE"
 $B > gpurun_out/ncu_plain_$TAG.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stream -s 1 -c 1 -o gpurun_out/prof_c4_$TAG $B > gpurun_out/ncu_full_$TAG.log 2>&1
 L="python bench.py --steps 3 --warmup 3 --no-cpu"

@@ -55,12 +55,14 @@ if __name__ == "__main__":
     ap.add_argument("rep")
     ap.add_argument("--workload", default=None)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--tile-name", default=None, help="variant name (rtm_tile_name) profiled")
     a = ap.parse_args()
     res = summary(a.rep)
     if a.workload:  # bench-consumable record for the dominant (first) kernel
         k = res[0]
         rd, wr = _scale(k["dram__bytes_read.sum"]), _scale(k["dram__bytes_write.sum"])
-        res = {"workload": a.workload, "report": a.rep.split("/")[-1], "kernel": k["kernel"],
+        res = {"workload": a.workload, "tile": a.tile_name, "report": a.rep.split("/")[-1],
+               "kernel": k["kernel"],
                "dram_bytes_per_launch": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
                "duration_ms": _num(k["gpu__time_duration.sum"]), "detail": k}
     txt = json.dumps(res, indent=1)
