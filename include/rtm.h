@@ -124,8 +124,13 @@ const char* rtm_tile_name(int tile_id);  /* e.g. "stream64x32k10d0"; NULL for un
  *   RTM_OPT_GRAPHS     1 (default) = capture runs of 16 steps in CUDA graphs, 0 = direct launches
  *   RTM_OPT_SHOT_ORDER batched contexts: 0 auto (shot-major when C fits in 40% of L2), 1 shot-major
  *                      (each shot's tiles co-run), 2 shot-fastest (co-running CTAs share C tiles)
+ *   RTM_OPT_HALO_MODE  in-process multi-slab contexts: 0 (default) boundary planes first + halo copies
+ *                      on copy engines overlapped with the interior; 1 fused push — one kernel per
+ *                      slab whose epilogue stores the boundary planes straight into the neighbours'
+ *                      halos (peer stores over NVLink; needs peer access, else RTM_EINVAL)
  * Unknown key or out-of-range value -> RTM_EINVAL.  rtm_get_option returns -1 for unknown keys. */
-enum { RTM_OPT_ZCHUNK = 1, RTM_OPT_CACHE_MODE = 2, RTM_OPT_GRAPHS = 3, RTM_OPT_SHOT_ORDER = 4 };
+enum { RTM_OPT_ZCHUNK = 1, RTM_OPT_CACHE_MODE = 2, RTM_OPT_GRAPHS = 3, RTM_OPT_SHOT_ORDER = 4,
+       RTM_OPT_HALO_MODE = 5 };
 int rtm_set_option(rtm_ctx* ctx, int key, long long value);
 long long rtm_get_option(rtm_ctx* ctx, int key);
 

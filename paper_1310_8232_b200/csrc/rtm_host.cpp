@@ -88,7 +88,7 @@ struct Slab {
     std::vector<float> h_samples;
     cudaStream_t s_own = nullptr, s_comm = nullptr, s_user = nullptr;
     bool has_user = false;
-    cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
+    cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr, ev_done = nullptr;
     CUtensorMap tm_u[2];   // u with the halo box, one per time-level buffer
     CUtensorMap tm_in[2];  // TX x TY box over each buffer (u_prev read of k_stream)
     CUtensorMap tm_c;      // TX x TY box over C
@@ -118,6 +118,7 @@ struct rtm_ctx {
     int zchunk = 0;  // 0 = auto
     int cache_mode = 0x41;  // L2 prefetch of u_prev/C 4 planes ahead, evict_last (tuned)
     int shot_order = 0;     // 0 auto, 1 shot-major, 2 shot-fastest
+    int halo_mode = 0;      // multi-slab: 0 copy engines (cudaMemcpyPeerAsync), 1 fused push
     int l2_bytes = 0;
     bool graphs = true;
     std::vector<HostSource> sources;
@@ -209,6 +210,7 @@ int alloc_slab(rtm_ctx* c, Slab& s) {
     CK(cudaStreamCreateWithFlags(&s.s_comm, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&s.ev_bnd, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&s.ev_comm, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&s.ev_done, cudaEventDisableTiming));
     for (int b = 0; b < 2; ++b) CK(cudaMemsetAsync(s.buf[b], 0, nbuf * sizeof(float), s.s_own));
     CK(cudaMemsetAsync(s.C, 0, plane * s.nzl * sizeof(float), s.s_own));
     CK(cudaMemsetAsync(s.d_step, 0, 2 * sizeof(int), s.s_own));
@@ -228,6 +230,7 @@ void free_slab(Slab& s) {
     if (s.d_samples) cudaFree(s.d_samples);
     if (s.ev_bnd) cudaEventDestroy(s.ev_bnd);
     if (s.ev_comm) cudaEventDestroy(s.ev_comm);
+    if (s.ev_done) cudaEventDestroy(s.ev_done);
     if (s.s_own) cudaStreamDestroy(s.s_own);
     if (s.s_comm) cudaStreamDestroy(s.s_comm);
     s = Slab();
@@ -373,10 +376,13 @@ void fill_params(const rtm_ctx* c, const Slab& s, int parity, StencilParams& p) 
 
 // Launch the stencil on planes [b0,b0+l0) (+ [b1,b1+l1) if l1 > 0) of slab s.
 int launch_stencil(rtm_ctx* c, Slab& s, int parity, int b0, int l0, int b1, int l1,
-                   int write_next, cudaStream_t st) {
+                   int write_next, cudaStream_t st, float* push_lo = nullptr,
+                   float* push_hi = nullptr) {
     const int var = resolve_tile(c);
     StencilParams p;
     fill_params(c, s, parity, p);
+    p.push_lo = push_lo;
+    p.push_hi = push_hi;
     p.write_next = write_next;
     p.nranges = l1 > 0 ? 2 : 1;
     p.r_begin[0] = b0;
@@ -540,8 +546,44 @@ int exchange_nccl(rtm_ctx* c, int parity_next) {
     return RTM_OK;
 }
 
+// G > 1 step, fused halo push (f1): one launch per slab per step whose epilogue also stores
+// the boundary planes into the neighbours' z-halo (peer stores over NVLink between GPUs, plain
+// stores on one GPU).  Step n on slab r waits for step n-1 of r-1, r, r+1 to finish: their
+// pushes into r's halo (RAW) and their reads of the halo planes r is about to overwrite (WAR).
+int step_slabs_fused(rtm_ctx* c, int nsteps) {
+    const int G = (int)c->slabs.size();
+    const size_t plane = (size_t)c->nx * c->ny;
+    for (int k = 0; k < nsteps; ++k) {
+        const int parity = (int)(c->step & 1);
+        for (int r = 0; r < G; ++r) {
+            Slab& s = c->slabs[r];
+            CK(cudaSetDevice(s.dev));
+            for (int d = -1; d <= 1; d += 2)
+                if (r + d >= 0 && r + d < G) CK(cudaStreamWaitEvent(s.stream(), c->slabs[r + d].ev_done, 0));
+        }
+        for (int r = 0; r < G; ++r) {
+            Slab& s = c->slabs[r];
+            CK(cudaSetDevice(s.dev));
+            float* lo = s.lo_nb ? c->slabs[r - 1].buf[parity ^ 1] + (size_t)(c->slabs[r - 1].nzl + 5) * plane
+                                : nullptr;
+            float* hi = s.hi_nb ? c->slabs[r + 1].buf[parity ^ 1] : nullptr;
+            RET(launch_stencil(c, s, parity, 0, s.nzl, 0, 0, 1, s.stream(), lo, hi));
+            CK(cudaEventRecord(s.ev_done, s.stream()));
+        }
+        ++c->step;
+    }
+    for (int r = 0; r < G; ++r) {  // join: every push into r has landed when the step returns
+        Slab& s = c->slabs[r];
+        CK(cudaSetDevice(s.dev));
+        for (int d = -1; d <= 1; d += 2)
+            if (r + d >= 0 && r + d < G) CK(cudaStreamWaitEvent(s.stream(), c->slabs[r + d].ev_done, 0));
+    }
+    return RTM_OK;
+}
+
 // G > 1 step: boundary planes first, exchange on the comm stream, interior concurrently.
 int step_slabs(rtm_ctx* c, int nsteps) {
+    if (c->mode == 1 && c->halo_mode == 1) return step_slabs_fused(c, nsteps);
     const int G = (int)c->slabs.size();
     for (int k = 0; k < nsteps; ++k) {
         const int parity = (int)(c->step & 1);
@@ -1061,6 +1103,28 @@ int rtm_set_option(rtm_ctx* c, int key, long long value) {
             if (value < 0 || value > 2) return fail(RTM_EINVAL, "shot order %lld not in 0..2", value);
             c->shot_order = (int)value;
             break;
+        case RTM_OPT_HALO_MODE:
+            if (value < 0 || value > 1) return fail(RTM_EINVAL, "halo mode %lld not in 0..1", value);
+            if (value == 1 && c->mode != 1)
+                return fail(RTM_EINVAL, "the fused halo push needs an in-process multi-slab context");
+            if (value == 1) {  // every slab must be able to store into its neighbours' memory
+                for (size_t r = 0; r + 1 < c->slabs.size(); ++r) {
+                    const int a = c->slabs[r].dev, b = c->slabs[r + 1].dev;
+                    int ab = 1, ba = 1;
+                    if (a != b) {
+                        cudaDeviceCanAccessPeer(&ab, a, b);
+                        cudaDeviceCanAccessPeer(&ba, b, a);
+                    }
+                    if (!ab || !ba)
+                        return fail(RTM_EINVAL, "devices %d and %d have no peer access", a, b);
+                }
+            }
+            {  // switch cleanly: drain, and refill the halos of both levels from the owners
+                DeviceGuard g;
+                RET(sync_all(c));
+                c->halo_mode = (int)value;
+            }
+            break;
         default:
             return fail(RTM_EINVAL, "unknown option key %d", key);
     }
@@ -1075,6 +1139,7 @@ long long rtm_get_option(rtm_ctx* c, int key) {
         case RTM_OPT_CACHE_MODE: return c->cache_mode;
         case RTM_OPT_GRAPHS: return c->graphs ? 1 : 0;
         case RTM_OPT_SHOT_ORDER: return c->shot_order;
+        case RTM_OPT_HALO_MODE: return c->halo_mode;
         default: return -1;
     }
 }

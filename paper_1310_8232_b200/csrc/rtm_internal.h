@@ -38,6 +38,11 @@ struct StencilParams {
     int cache_mode;            // k_stream L2 policy knobs (see rtm_kernels.cu)
     int shot_major;            // 1: units ordered shot-slowest (each shot's tiles co-run);
                                // 0: shot-fastest (co-running CTAs share the C tile)
+    // fused halo push (f1, in-process multi-slab): when non-null, owned planes [0,5) are also
+    // stored to push_lo + z*plane and planes [nzl-5, nzl) to push_hi + (z-nzl+5)*plane — the
+    // neighbours' z-halo planes of their u^{n+1} buffers (peer or same-device pointers)
+    float* push_lo;
+    float* push_hi;
     int nsrc;
     DevSource src[RTM_MAX_SOURCES];
     const float* samples;

@@ -118,6 +118,12 @@ __device__ __forceinline__ float comp(const float4& v, int i) {
     return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
 }
 
+// Fused halo push: mirror a finished boundary-plane value into the neighbour slab's z-halo.
+__device__ __forceinline__ void push_halo4(const StencilParams& p, int z, long long col, float4 v) {
+    if (z < 5 && p.push_lo) st_stream4(p.push_lo + (long long)z * p.plane + col, v);
+    if (z >= p.nzl - 5 && p.push_hi) st_stream4(p.push_hi + (long long)(z - p.nzl + 5) * p.plane + col, v);
+}
+
 // Add the samples of the sources owned by this thread's 4-point column at plane z.
 __device__ __forceinline__ void add_sources(const StencilParams& p, uint64_t mask, int x, int z,
                                             float (&out)[4]) {
@@ -290,9 +296,11 @@ __global__ void __launch_bounds__(TX * TY / 4, MINB)
             out[k] = rtm_point(zl, yl, xl, comp(upv, k), comp(cv, k), c);
         }
         if (smask) add_sources(p, smask, x, z, out);
-        if (active)
-            st_stream4(p.next + (soff + z + 5) * p.plane + col,
-                       make_float4(out[0], out[1], out[2], out[3]));
+        if (active) {
+            const float4 o4 = make_float4(out[0], out[1], out[2], out[3]);
+            st_stream4(p.next + (soff + z + 5) * p.plane + col, o4);
+            push_halo4(p, z, col, o4);
+        }
 
 #pragma unroll
         for (int o = 0; o < 10; ++o) q[o] = q[o + 1];
@@ -347,6 +355,8 @@ __global__ void __launch_bounds__(256) k_naive(const __grid_constant__ StencilPa
             }
         }
         p.next[pb] = out;
+        if (z < 5 && p.push_lo) p.push_lo[(long long)z * p.plane + inplane] = out;
+        if (z >= p.nzl - 5 && p.push_hi) p.push_hi[(long long)(z - p.nzl + 5) * p.plane + inplane] = out;
     }
 }
 
@@ -721,7 +731,11 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
                 if constexpr (D > 0) mbar_arrive_u32(ec + 8 * sq);
             }
             if (smask) add_sources(p, smask, x, g.zs + it, out);
-            if (active) st_mode4(outp, make_float4(out[0], out[1], out[2], out[3]), plain);
+            if (active) {
+                const float4 o4 = make_float4(out[0], out[1], out[2], out[3]);
+                st_mode4(outp, o4, plain);
+                if (p.push_lo || p.push_hi) push_halo4(p, g.zs + it, col, o4);
+            }
             if (++sn == K) sn = 0, pn ^= 1;
             if (++sc == K) sc = 0;
             if constexpr (D > 0) {

@@ -17,7 +17,7 @@ _LIB_PATH = Path(__file__).resolve().parent / "librtm_b200.so"
 
 RTM_OK, RTM_EINVAL, RTM_ECFL, RTM_ENOMEM, RTM_ECUDA, RTM_ENCCL, RTM_ESTATE = 0, -1, -2, -3, -4, -5, -6
 RTM_MAX_SOURCES = 64
-RTM_OPT_ZCHUNK, RTM_OPT_CACHE_MODE, RTM_OPT_GRAPHS, RTM_OPT_SHOT_ORDER = 1, 2, 3, 4
+RTM_OPT_ZCHUNK, RTM_OPT_CACHE_MODE, RTM_OPT_GRAPHS, RTM_OPT_SHOT_ORDER, RTM_OPT_HALO_MODE = 1, 2, 3, 4, 5
 _NAMES = {0: "RTM_OK", -1: "RTM_EINVAL", -2: "RTM_ECFL", -3: "RTM_ENOMEM", -4: "RTM_ECUDA",
           -5: "RTM_ENCCL", -6: "RTM_ESTATE"}
 

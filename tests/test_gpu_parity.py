@@ -175,8 +175,8 @@ def test_graph_and_direct_launch_paths_agree(P):
 
 
 # ----------------------------------------------------------------------------- slabs
-@pytest.mark.parametrize("G", [2, 3, 4])
-def test_multislab_on_one_gpu_bitwise_equals_single(P, G):
+@pytest.mark.parametrize("G,halo", [(2, 0), (3, 0), (4, 0), (2, 1), (3, 1), (4, 1)])
+def test_multislab_on_one_gpu_bitwise_equals_single(P, G, halo):
     """z-slab decomposition (boundary planes first, halo copies, interior) on one GPU gives
     exactly the G=1 field (R14)."""
     nz, ny, nx = 47, 33, 72
@@ -187,7 +187,16 @@ def test_multislab_on_one_gpu_bitwise_equals_single(P, G):
     bounds = [P.rtm_slab_range(nz, G, r)[0] for r in range(1, G)]
     src = [(5, 6, b, w) for b in bounds] + [(7, 8, b - 1, -w) for b in bounds] + [(1, 1, 0, w)]
     ref = gpu_run(P, v, 10.0, 1e-3, 9, u0=u0, up0=up0, sources=src)
-    got = gpu_run(P, v, 10.0, 1e-3, 9, u0=u0, up0=up0, sources=src, devices=[0] * G)
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, devices=[0] * G) as sim:
+        P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, halo)
+        assert P.rtm_get_option(sim.h, P.RTM_OPT_HALO_MODE) == halo
+        sim.set_velocity(v)
+        for s in src:
+            sim.inject_source(*s)
+        sim.set_fields(u0, up0)
+        sim.step(4)
+        sim.step(5)
+        got = sim.read_field()
     assert np.array_equal(got, ref)
     orc = oracle.run(v, 10.0, 1e-3, C32, 9, u0=u0, up0=up0, sources=src)
     assert relerr(got, orc) <= TOL_1 * 10
@@ -454,3 +463,9 @@ def test_batch_errors(P):
             P.rtm_inject_source_shot(h, 2, 1, 1, 1, np.ones(3, np.float32))
     finally:
         P.rtm_destroy(h)
+
+
+def test_fused_halo_mode_rejected_without_slabs(P):
+    with P.Simulation(16, 16, 16, 10.0, 1e-3, C32) as sim:
+        with pytest.raises(P.RtmError):
+            P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, 1)
