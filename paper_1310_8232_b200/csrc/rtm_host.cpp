@@ -1093,7 +1093,7 @@ int rtm_set_option(rtm_ctx* c, int key, long long value) {
             c->zchunk = (int)value;
             break;
         case RTM_OPT_CACHE_MODE:
-            if (value < 0 || value > 0x3ff) return fail(RTM_EINVAL, "cache mode %lld out of range", value);
+            if (value < 0 || value > 0x7ff) return fail(RTM_EINVAL, "cache mode %lld out of range", value);
             c->cache_mode = (int)value;
             break;
         case RTM_OPT_GRAPHS:

@@ -465,7 +465,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 // cache_mode (StencilParams): bits 0-1 L2 prefetch of u_prev/C (0 none, 1 evict_last,
 // 2 evict_normal); bit 2 u TMA loads with an evict_last L2 policy; bit 3 plain (not
-// evict-first) u_prev/C loads and u_next stores; bits 4-7 prefetch distance in planes.
+// evict-first) u_prev/C loads and u_next stores; bits 4-7 prefetch distance in planes;
+// bits 8-9 L2 promotion of the u box (host side); bit 10 u_prev/C TMA loads evict_first.
 __device__ __forceinline__ void prefetch_l2(const void* p, int mode) {
     if (mode == 1)
         asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
@@ -484,6 +485,11 @@ __device__ __forceinline__ void st_mode4(float* p, float4 v, bool plain) {
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
 __device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* tm, int x, int y,
@@ -567,7 +573,9 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
     if (warp == S::NW) {  // ---------------- producer warp
         if (lane == 0) {
             const bool hint = (p.cache_mode & 4) != 0;
+            const bool chint = (p.cache_mode & 0x400) != 0;
             const uint64_t pol = policy_evict_last();
+            const uint64_t cpol = policy_evict_first();
             uint32_t gu = 0, gc = 0;
             for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
                 const UnitGeom g = unit_geom(p, unit, TX, TY);
@@ -588,8 +596,15 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
                     if (seq >= D) mbar_wait(&empty_c[slot], ((seq / D) - 1) & 1);
                     mbar_expect_tx(&full_c[slot], S::CBYTES);
                     float* dst = cring + slot * S::CSLOT;
-                    tma_load_3d(dst, &tm_up, g.x0, g.y0, (int)g.soff + g.zs + i + 5, &full_c[slot]);
-                    tma_load_3d(dst + TX * TY, &tm_c, g.x0, g.y0, g.zs + i, &full_c[slot]);
+                    if (chint) {  // read-once streams: evict first, keep u's halo rows in L2
+                        tma_load_3d_hint(dst, &tm_up, g.x0, g.y0, (int)g.soff + g.zs + i + 5,
+                                         &full_c[slot], cpol);
+                        tma_load_3d_hint(dst + TX * TY, &tm_c, g.x0, g.y0, g.zs + i, &full_c[slot],
+                                         cpol);
+                    } else {
+                        tma_load_3d(dst, &tm_up, g.x0, g.y0, (int)g.soff + g.zs + i + 5, &full_c[slot]);
+                        tma_load_3d(dst + TX * TY, &tm_c, g.x0, g.y0, g.zs + i, &full_c[slot]);
+                    }
                 };
                 for (int j = 0; j < 10; ++j) put_u(j);
                 for (int i = 0; i < n; ++i) {
