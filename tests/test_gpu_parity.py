@@ -469,3 +469,71 @@ def test_fused_halo_mode_rejected_without_slabs(P):
     with P.Simulation(16, 16, 16, 10.0, 1e-3, C32) as sim:
         with pytest.raises(P.RtmError):
             P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, 1)
+
+
+# ----------------------------------------------------------------------------- full-size properties
+def _star_L_f64(u):
+    """L(u) in fp64 with the zero halo (independent numpy evaluation, plane-chunked)."""
+    nz, ny, nx = u.shape
+    c = ri.COEFFS_F64
+    out = np.zeros(u.shape, np.float64)
+    out += 3 * c[0] * u
+    for m in range(1, 6):
+        out[m:] += c[m] * u[:-m]
+        out[:-m] += c[m] * u[m:]
+        out[:, m:] += c[m] * u[:, :-m]
+        out[:, :-m] += c[m] * u[:, m:]
+        out[:, :, m:] += c[m] * u[:, :, :-m]
+        out[:, :, :-m] += c[m] * u[:, :, m:]
+    return out
+
+
+def _energy(u1, u0, Cf):
+    """E^{n+1/2} = sum (u^{n+1}-u^n)^2 / C - sum u^{n+1} L u^n."""
+    d = u1.astype(np.float64) - u0
+    return float(np.sum(d * d / Cf) - np.sum(u1.astype(np.float64) * _star_L_f64(u0.astype(np.float64))))
+
+
+def test_full_size_c3_energy_conserved_over_200_steps(P):
+    """C3 at full size (512^3) for its full 200 steps from random ICs without sources: the
+    discrete energy of the scheme (conserved exactly in real arithmetic for symmetric L and
+    any C > 0) drifts only by fp32 rounding.  A dropped/extra term, a wrong index in any
+    kernel path or a mis-staged tile breaks conservation at O(1)."""
+    cfg = ri.make_config(3)
+    v = cfg.velocity()
+    Cf = (v.astype(np.float64) * cfg.dt / cfg.dx) ** 2
+    u0, up0 = ri.random_fields(v.shape, seed=303, scale=1e-2)
+    with P.Simulation(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, C32) as sim:
+        sim.set_velocity(v)
+        sim.set_fields(u0, up0)
+        sim.step(1)
+        a1, a0 = sim.read_fields()
+        e_start = _energy(a1, a0, Cf)
+        sim.step(cfg.steps - 1)
+        b1, b0 = sim.read_fields()
+        e_end = _energy(b1, b0, Cf)
+    assert e_start > 0
+    assert abs(e_end - e_start) <= 1e-4 * e_start, (e_start, e_end)
+
+
+def test_full_size_c4_autotuned_variant_one_step_sampled(P):
+    """The launch configuration bench.py times: rtm_autotune over the stream variants on the
+    full C4 grid, then one step from random ICs with the selected variant, sampled against
+    the oracle point evaluator."""
+    cfg = ri.make_config(4)
+    v = cfg.velocity()
+    u0, up0 = ri.random_fields(v.shape, seed=44)
+    with P.Simulation(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, C32) as sim:
+        sim.set_velocity(v)
+        cands = [t for t in range(P.rtm_num_tiles()) if P.rtm_tile_name(t).startswith("stream")]
+        res, _ = P.rtm_autotune(sim.h, 2, tiles=cands)
+        assert sim.tile == res["best_tile"]
+        sim.set_fields(u0, up0)
+        sim.step(1)
+        got = sim.read_field()
+    rng = np.random.default_rng(404)
+    nz, ny, nx = v.shape
+    pts = np.stack([rng.integers(0, nx, 100_000), rng.integers(0, ny, 100_000),
+                    rng.integers(0, nz, 100_000)], 1).astype(np.int32)
+    ref = oracle.points_f32(v, cfg.dx, cfg.dt, C32, u0, up0, pts)
+    assert relerr(got[pts[:, 2], pts[:, 1], pts[:, 0]], ref) <= TOL_1
