@@ -44,7 +44,8 @@ enum {
     RTM_ENOMEM = -3, /* device or host allocation failed                                    */
     RTM_ECUDA = -4,  /* a CUDA runtime/driver call or kernel failed                          */
     RTM_ENCCL = -5,  /* an NCCL call failed                                                  */
-    RTM_ESTATE = -6  /* call not valid in this state (e.g. rtm_step before rtm_set_velocity) */
+    RTM_ESTATE = -6, /* call not valid in this state (e.g. rtm_step before rtm_set_velocity) */
+    RTM_EUNSTABLE = -7 /* the field check (RTM_OPT_CHECK_EVERY) found a non-finite value      */
 };
 
 #define RTM_MAX_SOURCES 64
@@ -95,6 +96,13 @@ int rtm_read_fields(rtm_ctx* ctx, float* u, float* u_prev);
 int rtm_reset(rtm_ctx* ctx);
 /* Number of steps taken since the last reset / set_fields. */
 long long rtm_step_count(rtm_ctx* ctx);
+/* Checkpoint / resume: after rtm_set_fields(u^n, u^{n-1}) of a saved state, set the step index
+ * n so source samples continue at samples[n] (n >= 0). */
+int rtm_set_step_count(rtm_ctx* ctx, long long n);
+/* Failure detection: max |u^n| and the number of non-finite values of the current field
+ * (device reduction; all slabs).  With RTM_OPT_CHECK_EVERY = k > 0, rtm_step runs this check
+ * every k steps and returns RTM_EUNSTABLE at the first non-finite value. */
+int rtm_field_stats(rtm_ctx* ctx, double* max_abs, long long* nonfinite);
 
 /* Device-resident variants (the bench's kernel-only leg): d_v / d_out are device pointers
  * on the context's device (single-slab contexts only), same layout as the host versions.
@@ -125,13 +133,14 @@ const char* rtm_tile_name(int tile_id);  /* e.g. "stream64x32k10d0"; NULL for un
  *   RTM_OPT_GRAPHS     1 (default) = capture runs of 16 steps in CUDA graphs, 0 = direct launches
  *   RTM_OPT_SHOT_ORDER batched contexts: 0 auto (shot-major when C fits in 40% of L2), 1 shot-major
  *                      (each shot's tiles co-run), 2 shot-fastest (co-running CTAs share C tiles)
+ *   RTM_OPT_CHECK_EVERY 0 (default) off; k > 0: rtm_step checks the field for NaN/Inf every k steps
  *   RTM_OPT_HALO_MODE  in-process multi-slab contexts: 0 (default) boundary planes first + halo copies
  *                      on copy engines overlapped with the interior; 1 fused push — one kernel per
  *                      slab whose epilogue stores the boundary planes straight into the neighbours'
  *                      halos (peer stores over NVLink; needs peer access, else RTM_EINVAL)
  * Unknown key or out-of-range value -> RTM_EINVAL.  rtm_get_option returns -1 for unknown keys. */
 enum { RTM_OPT_ZCHUNK = 1, RTM_OPT_CACHE_MODE = 2, RTM_OPT_GRAPHS = 3, RTM_OPT_SHOT_ORDER = 4,
-       RTM_OPT_HALO_MODE = 5 };
+       RTM_OPT_HALO_MODE = 5, RTM_OPT_CHECK_EVERY = 6 };
 int rtm_set_option(rtm_ctx* ctx, int key, long long value);
 long long rtm_get_option(rtm_ctx* ctx, int key);
 

@@ -119,6 +119,7 @@ struct rtm_ctx {
     int cache_mode = 0x41;  // L2 prefetch of u_prev/C 4 planes ahead, evict_last (tuned)
     int shot_order = 0;     // 0 auto, 1 shot-major, 2 shot-fastest
     int halo_mode = 0;      // multi-slab: 0 copy engines (cudaMemcpyPeerAsync), 1 fused push
+    int check_every = 0;    // NaN/Inf scan every k steps (0 = off)
     int l2_bytes = 0;
     bool graphs = true;
     std::vector<HostSource> sources;
@@ -989,6 +990,26 @@ int rtm_step(rtm_ctx* c, int nsteps) {
     Slab& s0 = c->slabs[0];
     CK(cudaSetDevice(s0.dev));
     c->prof_launches = 0;
+    if (c->check_every > 0) {  // failure detection: advance in blocks, scan between them
+        int left = nsteps;
+        while (left > 0) {
+            const long long to_boundary = c->check_every - (c->step % c->check_every);
+            const int k = (int)std::min<long long>(left, to_boundary);
+            c->check_every = -c->check_every;  // run the block unchecked
+            const int rc = rtm_step(c, k);
+            c->check_every = -c->check_every;
+            if (rc != RTM_OK) return rc;
+            left -= k;
+            if (c->step % c->check_every == 0) {
+                double m;
+                long long bad;
+                RET(rtm_field_stats(c, &m, &bad));
+                if (bad)
+                    return fail(RTM_EUNSTABLE, "%lld non-finite values in u at step %lld", bad, c->step);
+            }
+        }
+        return RTM_OK;
+    }
     CK(cudaEventRecord(c->t0, s0.stream()));
     if (c->mode == 0) {
         RET(step_single(c, nsteps));
@@ -1064,6 +1085,51 @@ int rtm_reset(rtm_ctx* c) {
 
 long long rtm_step_count(rtm_ctx* c) { return c ? c->step : -1; }
 
+int rtm_set_step_count(rtm_ctx* c, long long n) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    if (n < 0 || n > (1LL << 30)) return fail(RTM_EINVAL, "step index %lld out of range", n);
+    DeviceGuard g;
+    RET(sync_all(c));
+    // the time levels stay where rtm_set_fields put them (u in buf[0], u_prev in buf[1]): if
+    // the parity of n is odd, swap so that u^n lives in buf[n & 1]
+    if ((n & 1) != (c->step & 1))
+        for (auto& s : c->slabs) {
+            std::swap(s.buf[0], s.buf[1]);
+            s.tm_variant = -1;  // tensor maps follow the buffers
+            s.graph_valid = false;
+        }
+    for (auto& s : c->slabs) {
+        CK(cudaSetDevice(s.dev));
+        int h[2] = {(int)n, (int)n};
+        CK(cudaMemcpy(s.d_step, h, sizeof h, cudaMemcpyHostToDevice));
+    }
+    c->step = n;
+    return RTM_OK;
+}
+
+int rtm_field_stats(rtm_ctx* c, double* max_abs, long long* nonfinite) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    DeviceGuard g;
+    const long long plane = (long long)c->nx * c->ny;
+    double m = 0;
+    long long bad = 0;
+    for (auto& s : c->slabs) {
+        CK(cudaSetDevice(s.dev));
+        CK(cudaMemsetAsync(s.d_stats, 0, 2 * sizeof(unsigned int), s.stream()));
+        CK(launch_field_stats(s.buf[c->step & 1], plane, s.nzl, s.nshots, s.d_stats, s.stream()));
+        unsigned int h[2];
+        CK(cudaMemcpyAsync(h, s.d_stats, sizeof h, cudaMemcpyDeviceToHost, s.stream()));
+        CK(cudaStreamSynchronize(s.stream()));
+        float f;
+        std::memcpy(&f, &h[0], 4);
+        m = std::max(m, (double)f);
+        bad += h[1];
+    }
+    if (max_abs) *max_abs = m;
+    if (nonfinite) *nonfinite = bad;
+    return RTM_OK;
+}
+
 int rtm_set_tile(rtm_ctx* c, int tile_id) {
     if (!c) return fail(RTM_EINVAL, "ctx is NULL");
     if (tile_id < -1 || tile_id >= num_variants())
@@ -1103,6 +1169,10 @@ int rtm_set_option(rtm_ctx* c, int key, long long value) {
             if (value < 0 || value > 2) return fail(RTM_EINVAL, "shot order %lld not in 0..2", value);
             c->shot_order = (int)value;
             break;
+        case RTM_OPT_CHECK_EVERY:
+            if (value < 0 || value > (1 << 30)) return fail(RTM_EINVAL, "check interval %lld", value);
+            c->check_every = (int)value;
+            break;
         case RTM_OPT_HALO_MODE:
             if (value < 0 || value > 1) return fail(RTM_EINVAL, "halo mode %lld not in 0..1", value);
             if (value == 1 && c->mode != 1)
@@ -1140,6 +1210,7 @@ long long rtm_get_option(rtm_ctx* c, int key) {
         case RTM_OPT_GRAPHS: return c->graphs ? 1 : 0;
         case RTM_OPT_SHOT_ORDER: return c->shot_order;
         case RTM_OPT_HALO_MODE: return c->halo_mode;
+        case RTM_OPT_CHECK_EVERY: return c->check_every;
         default: return -1;
     }
 }

@@ -72,6 +72,10 @@ cudaError_t launch_naive(const StencilParams& p, cudaStream_t s);
 
 // a1: C = fp32((double(v)*dt/dx)^2), stats[0] = max(v) bits (v > 0), stats[1] = count of
 // invalid (non-finite or <= 0) velocities.  v and C may alias.
+// Field check: stats[0] = max |u| bits (uint order of non-negative floats), stats[1] = number of
+// non-finite values, over the owned planes of every shot in a slab buffer.
+cudaError_t launch_field_stats(const float* buf, long long plane, int nzl, int nshots,
+                               unsigned int* stats, cudaStream_t s);
 cudaError_t launch_velocity(const float* v, float* C, long long n, double dt, double dx,
                             unsigned int* stats, cudaStream_t s);
 

@@ -900,6 +900,40 @@ cudaError_t launch_naive(const StencilParams& p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+__global__ void __launch_bounds__(256) k_field_stats(const float* buf, long long plane, int nzl,
+                                                     int nshots, unsigned int* stats) {
+    float m = 0.0f;
+    unsigned int bad = 0;
+    const long long per_shot = plane * nzl;
+    const long long n = per_shot * nshots;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long shot = t / per_shot;
+        const float v = buf[(shot * (nzl + 10) + 5) * plane + (t - shot * per_shot)];
+        if (!isfinite(v)) ++bad;
+        else m = fmaxf(m, fabsf(v));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&stats[0], __float_as_uint(m));
+        if (bad) atomicAdd(&stats[1], bad);
+    }
+}
+
+cudaError_t launch_field_stats(const float* buf, long long plane, int nzl, int nshots,
+                               unsigned int* stats, cudaStream_t s) {
+    const long long n = plane * nzl * nshots;
+    if (n <= 0) return cudaSuccess;
+    long long blocks = (n + 255) / 256;
+    if (blocks > 148LL * 8) blocks = 148LL * 8;
+    k_field_stats<<<static_cast<unsigned>(blocks), 256, 0, s>>>(buf, plane, nzl, nshots, stats);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_velocity(const float* v, float* C, long long n, double dt, double dx,
                             unsigned int* stats, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;

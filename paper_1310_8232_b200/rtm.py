@@ -16,10 +16,12 @@ import numpy as np
 _LIB_PATH = Path(__file__).resolve().parent / "librtm_b200.so"
 
 RTM_OK, RTM_EINVAL, RTM_ECFL, RTM_ENOMEM, RTM_ECUDA, RTM_ENCCL, RTM_ESTATE = 0, -1, -2, -3, -4, -5, -6
+RTM_EUNSTABLE = -7
 RTM_MAX_SOURCES = 64
 RTM_OPT_ZCHUNK, RTM_OPT_CACHE_MODE, RTM_OPT_GRAPHS, RTM_OPT_SHOT_ORDER, RTM_OPT_HALO_MODE = 1, 2, 3, 4, 5
+RTM_OPT_CHECK_EVERY = 6
 _NAMES = {0: "RTM_OK", -1: "RTM_EINVAL", -2: "RTM_ECFL", -3: "RTM_ENOMEM", -4: "RTM_ECUDA",
-          -5: "RTM_ENCCL", -6: "RTM_ESTATE"}
+          -5: "RTM_ENCCL", -6: "RTM_ESTATE", -7: "RTM_EUNSTABLE"}
 
 
 class RtmError(RuntimeError):
@@ -52,6 +54,8 @@ _SIGS = {
     "rtm_read_fields": (_I, [_P, _P, _P]),
     "rtm_reset": (_I, [_P]),
     "rtm_step_count": (_LL, [_P]),
+    "rtm_set_step_count": (_I, [_P, _LL]),
+    "rtm_field_stats": (_I, [_P, ctypes.POINTER(_D), ctypes.POINTER(_LL)]),
     "rtm_set_velocity_device": (_I, [_P, _P]),
     "rtm_read_field_device": (_I, [_P, _P]),
     "rtm_set_tile": (_I, [_P, _I]),
@@ -168,6 +172,16 @@ def rtm_reset(h):
 
 def rtm_step_count(h) -> int:
     return int(lib.rtm_step_count(h))
+
+
+def rtm_set_step_count(h, n):
+    return _check(lib.rtm_set_step_count(h, int(n)))
+
+
+def rtm_field_stats(h):
+    m, bad = _D(0), _LL(0)
+    _check(lib.rtm_field_stats(h, ctypes.byref(m), ctypes.byref(bad)))
+    return float(m.value), int(bad.value)
 
 
 def rtm_set_velocity_device(h, dptr: int):

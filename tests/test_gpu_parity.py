@@ -537,3 +537,46 @@ def test_full_size_c4_autotuned_variant_one_step_sampled(P):
                     rng.integers(0, nz, 100_000)], 1).astype(np.int32)
     ref = oracle.points_f32(v, cfg.dx, cfg.dt, C32, u0, up0, pts)
     assert relerr(got[pts[:, 2], pts[:, 1], pts[:, 0]], ref) <= TOL_1
+
+
+# ----------------------------------------------------------------------------- resume / failure detection
+@pytest.mark.parametrize("n0", [30, 31])
+def test_checkpoint_resume_bitwise(P, n0):
+    cfg = ri.make_config(2, shape=(40, 36, 64), steps=50)
+    v = cfg.velocity()
+    src = cfg.sources()
+    ref = gpu_run(P, v, cfg.dx, cfg.dt, 50, sources=src)
+    with P.Simulation(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, C32) as sim:
+        sim.set_velocity(v)
+        for s in src:
+            sim.inject_source(*s)
+        sim.step(n0)
+        u, up = sim.read_fields()
+    with P.Simulation(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, C32) as sim:
+        sim.set_velocity(v)
+        for s in src:
+            sim.inject_source(*s)
+        sim.set_fields(u, up)
+        P.rtm_set_step_count(sim.h, n0)
+        assert sim.steps_taken == n0
+        sim.step(50 - n0)
+        assert np.array_equal(sim.read_field(), ref)
+
+
+def test_field_stats_and_instability_detection(P):
+    shape = (20, 24, 32)
+    v = np.full(shape, 3000.0, np.float32)
+    u0, up0 = ri.random_fields(shape, seed=6)
+    with P.Simulation(32, 24, 20, 10.0, 1e-3, C32) as sim:
+        sim.set_velocity(v)
+        sim.set_fields(u0, up0)
+        m, bad = P.rtm_field_stats(sim.h)
+        assert bad == 0 and m == pytest.approx(float(np.abs(u0).max()))
+        P.rtm_set_option(sim.h, P.RTM_OPT_CHECK_EVERY, 3)
+        sim.step(7)  # finite: no error
+        u0[10, 12, 16] = np.inf
+        sim.set_fields(u0, up0)
+        with pytest.raises(P.RtmError) as e:
+            sim.step(5)
+        assert e.value.code == P.RTM_EUNSTABLE
+        assert sim.steps_taken == 3  # stopped at the first check
