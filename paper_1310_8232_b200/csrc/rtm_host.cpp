@@ -288,7 +288,7 @@ int finish_ctx(rtm_ctx* c) {
 int resolve_tile(const rtm_ctx* c) {
     if (c->nx % 4 != 0) return 0;  // 128-bit rows / TMA strides need nx % 4 == 0
     if (c->tile >= 0) return c->tile;
-    return 13;  // stream64x16k8d4u11: best on C4 (profiles/sweep_c4_u1.log)
+    return 35;  // stream64x30k10d6u4: best on C4 (profiles/sweep_c4_s6.log); bench autotunes
 }
 
 int encode_3d(CUtensorMap* tm, void* base, int nx, int ny, int nplanes, int bx, int by,
@@ -410,8 +410,8 @@ int launch_stencil(rtm_ctx* c, Slab& s, int parity, int b0, int l0, int b1, int 
         p.tiles_x = (c->nx + tv.TX - 1) / tv.TX;
         p.tiles_y = (c->ny + tv.TY - 1) / tv.TY;
         const int nt = p.tiles_x * p.tiles_y;
-        p.r_chunks[0] = choose_chunks(c, s.occupancy, nt, l0);
-        p.r_chunks[1] = l1 > 0 ? choose_chunks(c, s.occupancy, nt, l1) : 0;
+        p.r_chunks[0] = choose_chunks(c, s.occupancy, nt * s.nshots, l0);  // units = tiles x chunks x shots
+        p.r_chunks[1] = l1 > 0 ? choose_chunks(c, s.occupancy, nt * s.nshots, l1) : 0;
         CK(launch_variant(var, &s.tm_u[parity], &s.tm_in[parity ^ 1], &s.tm_c, p,
                           c->num_sms * s.occupancy, st));
     }

@@ -807,7 +807,17 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
     X(23, "stream64x14k9d6u4", 2, 64, 14, 9, 6, 2, 4)    \
     X(24, "stream64x14k8d7u4", 2, 64, 14, 8, 7, 2, 4)    \
     X(25, "stream32x28k10d5u4", 2, 32, 28, 10, 5, 2, 4)  \
-    X(26, "stream64x14k10d5u11", 2, 64, 14, 10, 5, 2, 11)
+    X(26, "stream64x14k10d5u11", 2, 64, 14, 10, 5, 2, 11) \
+    X(27, "stream64x28k10d4u4", 2, 64, 28, 10, 4, 1, 4)   \
+    X(28, "stream64x28k10d6u4", 2, 64, 28, 10, 6, 1, 4)   \
+    X(29, "stream128x14k9d5u4", 2, 128, 14, 9, 5, 1, 4)   \
+    X(30, "stream64x14k10d5u2", 2, 64, 14, 10, 5, 2, 2)   \
+    X(31, "stream64x28k11d6u4", 2, 64, 28, 11, 6, 1, 4)   \
+    X(32, "stream64x28k10d7u4", 2, 64, 28, 10, 7, 1, 4)   \
+    X(33, "stream128x14k10d6u4", 2, 128, 14, 10, 6, 1, 4) \
+    X(34, "stream64x24k11d7u4", 2, 64, 24, 11, 7, 1, 4)   \
+    X(35, "stream64x30k10d6u4", 2, 64, 30, 10, 6, 1, 4)   \
+    X(36, "stream64x28k10d6u11", 2, 64, 28, 10, 6, 1, 11)
 
 static const TileVariant kVariants[] = {
     {"naive", 0, 0, 0, 0, 0, 0, 1},
