@@ -23,13 +23,20 @@ def main():
     ap.add_argument("--repeat", type=int, default=1, help="interleaved repetitions (min is kept)")
     ap.add_argument("--shots", type=int, default=1)
     ap.add_argument("--shot-order", default="0", help="comma list of RTM_OPT_SHOT_ORDER values")
+    ap.add_argument("--slabs", type=int, default=1, help="in-process z-slabs (all on visible GPUs round-robin)")
+    ap.add_argument("--halo", type=int, default=0, help="RTM_OPT_HALO_MODE for --slabs > 1")
     args = ap.parse_args()
     import torch
     import paper_1310_8232_b200 as P
     import rtm_inputs as ri
     cfg = ri.make_config(args.config)
     v = cfg.velocity()
-    if args.shots > 1:
+    if args.slabs > 1:
+        ndev = torch.cuda.device_count()
+        h = P.rtm_create_multi(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32,
+                               [k % ndev for k in range(args.slabs)])
+        P.rtm_set_option(h, P.RTM_OPT_HALO_MODE, args.halo)
+    elif args.shots > 1:
         h = P.rtm_create_batch(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32, args.shots)
     else:
         h = P.rtm_create(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32)
@@ -37,7 +44,8 @@ def main():
     for s in cfg.sources(v):
         P.rtm_inject_source(h, *s)
     st = torch.cuda.Stream()
-    P.rtm_set_stream(h, st.cuda_stream)
+    if args.slabs == 1:
+        P.rtm_set_stream(h, st.cuda_stream)
     tiles = [int(t) for t in args.tiles.split(",")] if args.tiles else list(range(P.rtm_num_tiles()))
     res = []
     for t in [t for _ in range(args.repeat) for t in tiles]:
@@ -51,14 +59,19 @@ def main():
                 P.rtm_set_option(h, P.RTM_OPT_CACHE_MODE, cm)
             P.rtm_reset(h)
             P.rtm_step(h, 4)  # warm-up (graphs, tensor maps)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
-            P.rtm_step(h, args.ni)
-            e1.record(st)
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / args.ni
+            if args.slabs == 1:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                P.rtm_step(h, args.ni)
+                e1.record(st)
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / args.ni
+            else:  # the library's own CUDA-event time of the rtm_step call (all slabs joined)
+                P.rtm_step(h, args.ni)
+                ms = P.rtm_last_elapsed_ms(h) / args.ni
             gpts = cfg.points * args.shots / ms / 1e6
             r = {"tile": t, "name": P.rtm_tile_name(t), "zchunk": zc, "shot_order": so,
+                 "slabs": args.slabs, "halo": args.halo,
                  "cache": hex(P.rtm_get_option(h, P.RTM_OPT_CACHE_MODE)), "ms_per_step": round(ms, 4),
                  "gpts": round(gpts, 2), "eff_gbs": round(16 * gpts, 1)}
             res.append(r)
