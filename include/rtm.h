@@ -113,7 +113,11 @@ int rtm_read_field_device(rtm_ctx* ctx, float* d_out);
 /* Kernel variant ("tile", the GPU analogue of the paper's blocksize):
  * -1 = automatic (default), 0 = naive one-thread-per-point kernel, 1..rtm_num_tiles()-1 =
  * TMA-staged xy tiles.  Unknown id -> RTM_EINVAL.  Every variant computes bitwise-identical
- * results (one per-point expression). */
+ * results (one per-point expression).  Variants named "tb2_*" advance TWO time steps per HBM
+ * pass (temporal blocking) on single-GPU single-shot contexts: u^{n+1} is
+ * produced and consumed through L2 by co-resident CTAs of a y-band; the context then keeps a
+ * second pair of field buffers (2 x nx*ny*(nz+10) floats more).  Odd remainders, multi-slab
+ * and batched contexts run the variant's paired single-step kernel. */
 int rtm_set_tile(rtm_ctx* ctx, int tile_id);
 int rtm_get_tile(rtm_ctx* ctx);          /* the variant rtm_step will use (resolves -1) */
 int rtm_num_tiles(void);
@@ -138,9 +142,12 @@ const char* rtm_tile_name(int tile_id);  /* e.g. "stream64x32k10d0"; NULL for un
  *                      on copy engines overlapped with the interior; 1 fused push — one kernel per
  *                      slab whose epilogue stores the boundary planes straight into the neighbours'
  *                      halos (peer stores over NVLink; needs peer access, else RTM_EINVAL)
+ *   RTM_OPT_TB_CTAS    two-step variants ("tb2_*"): max CTAs per y-band launch,
+ *                      0 (default) = one per SM.  Smaller values force more, narrower bands
+ *                      (used by the tests to cover band edges on small grids).
  * Unknown key or out-of-range value -> RTM_EINVAL.  rtm_get_option returns -1 for unknown keys. */
 enum { RTM_OPT_ZCHUNK = 1, RTM_OPT_CACHE_MODE = 2, RTM_OPT_GRAPHS = 3, RTM_OPT_SHOT_ORDER = 4,
-       RTM_OPT_HALO_MODE = 5, RTM_OPT_CHECK_EVERY = 6 };
+       RTM_OPT_HALO_MODE = 5, RTM_OPT_CHECK_EVERY = 6, RTM_OPT_TB_CTAS = 7 };
 int rtm_set_option(rtm_ctx* ctx, int key, long long value);
 long long rtm_get_option(rtm_ctx* ctx, int key);
 

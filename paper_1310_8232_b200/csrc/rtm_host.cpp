@@ -97,7 +97,15 @@ struct Slab {
     cudaGraphExec_t graph = nullptr;
     cudaGraph_t graph_def = nullptr;
     int graph_variant = -1;
+    int graph_bank = 0;
     bool graph_valid = false;
+    // two-step passes (kind 3): the second bank they write, then the banks swap
+    float* alt[2] = {nullptr, nullptr};
+    int bank = 0;                              // toggled at every bank swap
+    unsigned long long* d_flags = nullptr;     // stage-A progress per CTA of a band
+    unsigned long long* d_epoch = nullptr;     // pass epoch (never reset)
+    cudaGraphExec_t tb_graph[4] = {nullptr, nullptr, nullptr, nullptr};  // key bank*2 + parity
+    int tb_graph_variant[4] = {-1, -1, -1, -1};
     cudaStream_t stream() const { return has_user ? s_user : s_own; }
 };
 
@@ -120,6 +128,7 @@ struct rtm_ctx {
     int shot_order = 0;     // 0 auto, 1 shot-major, 2 shot-fastest
     int halo_mode = 0;      // multi-slab: 0 copy engines (cudaMemcpyPeerAsync), 1 fused push
     int check_every = 0;    // NaN/Inf scan every k steps (0 = off)
+    int tb_ctas = 0;        // two-step passes: max CTAs per band (0 = #SMs)
     int l2_bytes = 0;
     bool graphs = true;
     std::vector<HostSource> sources;
@@ -223,8 +232,14 @@ void free_slab(Slab& s) {
     cudaSetDevice(s.dev);
     if (s.graph) cudaGraphExecDestroy(s.graph);
     if (s.graph_def) cudaGraphDestroy(s.graph_def);
-    for (int b = 0; b < 2; ++b)
+    for (auto& g : s.tb_graph)
+        if (g) cudaGraphExecDestroy(g);
+    for (int b = 0; b < 2; ++b) {
         if (s.buf[b]) cudaFree(s.buf[b]);
+        if (s.alt[b]) cudaFree(s.alt[b]);
+    }
+    if (s.d_flags) cudaFree(s.d_flags);
+    if (s.d_epoch) cudaFree(s.d_epoch);
     if (s.C) cudaFree(s.C);
     if (s.d_step) cudaFree(s.d_step);
     if (s.d_stats) cudaFree(s.d_stats);
@@ -289,6 +304,13 @@ int resolve_tile(const rtm_ctx* c) {
     if (c->nx % 4 != 0) return 0;  // 128-bit rows / TMA strides need nx % 4 == 0
     if (c->tile >= 0) return c->tile;
     return 35;  // stream64x30k10d6u4: best on C4 (profiles/sweep_c4_s6.log); bench autotunes
+}
+
+// The variant that runs single time steps: a two-step variant (kind 3) runs its paired
+// k_stream variant for odd remainders and for contexts it does not cover (slabs, shots).
+int single_variant(const rtm_ctx* c) {
+    const int v = resolve_tile(c);
+    return variant(v).kind == 3 ? variant(v).pair : v;
 }
 
 int encode_3d(CUtensorMap* tm, void* base, int nx, int ny, int nplanes, int bx, int by,
@@ -379,7 +401,7 @@ void fill_params(const rtm_ctx* c, const Slab& s, int parity, StencilParams& p) 
 int launch_stencil(rtm_ctx* c, Slab& s, int parity, int b0, int l0, int b1, int l1,
                    int write_next, cudaStream_t st, float* push_lo = nullptr,
                    float* push_hi = nullptr) {
-    const int var = resolve_tile(c);
+    const int var = single_variant(c);
     StencilParams p;
     fill_params(c, s, parity, p);
     p.push_lo = push_lo;
@@ -435,8 +457,8 @@ int collect_profile(rtm_ctx* c) {
 }
 
 int build_graph(rtm_ctx* c, Slab& s) {
-    const int var = resolve_tile(c);
-    if (s.graph_valid && s.graph_variant == var) return RTM_OK;
+    const int var = single_variant(c);
+    if (s.graph_valid && s.graph_variant == var && s.graph_bank == s.bank) return RTM_OK;
     if (s.graph) cudaGraphExecDestroy(s.graph), s.graph = nullptr;
     if (s.graph_def) cudaGraphDestroy(s.graph_def), s.graph_def = nullptr;
     RET(ensure_tmaps(c, s, var));
@@ -457,11 +479,177 @@ int build_graph(rtm_ctx* c, Slab& s) {
     CK(cudaGraphInstantiate(&s.graph, g, 0));
     s.graph_valid = true;
     s.graph_variant = var;
+    s.graph_bank = s.bank;
     return RTM_OK;
 }
 
 void invalidate_graphs(rtm_ctx* c) {
-    for (auto& s : c->slabs) s.graph_valid = false;
+    for (auto& s : c->slabs) {
+        s.graph_valid = false;
+        for (int k = 0; k < 4; ++k) s.tb_graph_variant[k] = -1;
+    }
+}
+
+// ---- two-step passes (kind 3, k_tb2 in rtm_tb.cu) ----------------------
+struct TBBand {
+    int ya_lo, ya_hi, yb_lo, yb_hi, tiles_y;
+};
+
+// y-bands of a single-slab single-shot grid for variant tv: each band's A region (its rows
+// + 5 each side, clipped to the grid) must fit the CTA grid tiles_x x tiles_y <= #SMs (one
+// resident CTA per SM).  Rows are split evenly over the fewest bands that fit.
+bool tb_plan(const rtm_ctx* c, const TileVariant& tv, int* tiles_x, std::vector<TBBand>* bands) {
+    if (c->mode != 0 || c->slabs.size() != 1 || c->slabs[0].nshots != 1 || c->nx % 4) return false;
+    const int tx = (c->nx + tv.TX - 1) / tv.TX;
+    const int ctas = c->tb_ctas > 0 ? std::min(c->tb_ctas, c->num_sms) : c->num_sms;
+    const int cap = ctas / tx;  // tile rows per band
+    if (cap < 1) return false;
+    const int R = cap * tv.TY;
+    int nb = 1;
+    if (R < c->ny) {
+        if (R <= 10) return false;
+        nb = (c->ny + (R - 10) - 1) / (R - 10);
+    }
+    bands->clear();
+    for (int b = 0; b < nb; ++b) {
+        TBBand t;
+        t.yb_lo = (int)((long long)b * c->ny / nb);
+        t.yb_hi = (int)((long long)(b + 1) * c->ny / nb);
+        t.ya_lo = std::max(0, t.yb_lo - 5);
+        t.ya_hi = std::min(c->ny, t.yb_hi + 5);
+        t.tiles_y = (t.ya_hi - t.ya_lo + tv.TY - 1) / tv.TY;
+        if (t.tiles_y > cap || t.yb_hi <= t.yb_lo) return false;
+        bands->push_back(t);
+    }
+    *tiles_x = tx;
+    return true;
+}
+
+bool tb_active(const rtm_ctx* c) {
+    const int v = resolve_tile(c);
+    if (variant(v).kind != 3) return false;
+    int tx;
+    std::vector<TBBand> b;
+    return tb_plan(c, variant(v), &tx, &b);
+}
+
+int tb_alloc(rtm_ctx* c, Slab& s) {
+    if (s.alt[0]) return RTM_OK;
+    CK(cudaSetDevice(s.dev));
+    const size_t nbuf = (size_t)c->nx * c->ny * s.buf_planes();
+    for (int b = 0; b < 2; ++b) {
+        if (cudaMalloc(&s.alt[b], nbuf * sizeof(float)) != cudaSuccess) {
+            cudaGetLastError();
+            if (s.alt[0]) cudaFree(s.alt[0]), s.alt[0] = nullptr;
+            return fail(RTM_ENOMEM, "cudaMalloc of %zu bytes (two-step bank %d) failed", nbuf * 4, b);
+        }
+        CK(cudaMemsetAsync(s.alt[b], 0, nbuf * sizeof(float), s.stream()));  // z-halo planes stay 0
+    }
+    CK(cudaMalloc(&s.d_flags, (size_t)c->num_sms * sizeof(unsigned long long)));
+    CK(cudaMalloc(&s.d_epoch, sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(s.d_flags, 0, (size_t)c->num_sms * sizeof(unsigned long long), s.stream()));
+    CK(cudaMemsetAsync(s.d_epoch, 0, sizeof(unsigned long long), s.stream()));
+    CK(cudaStreamSynchronize(s.stream()));
+    return RTM_OK;
+}
+
+// One pass n -> n+2 (parity = n & 1): stage A reads u^n = buf[parity], u^{n-1} = buf[parity^1]
+// and writes u^{n+1} to alt[parity^1]; stage B writes u^{n+2} to alt[parity]; then the banks
+// swap so that u^{n+2} is buf[parity] again (u^m always lives in buf[m & 1]).
+int tb_pass(rtm_ctx* c, Slab& s, int parity, cudaStream_t st) {
+    const int var = resolve_tile(c);
+    const TileVariant& tv = variant(var);
+    int tiles_x;
+    std::vector<TBBand> bands;
+    if (!tb_plan(c, tv, &tiles_x, &bands)) return fail(RTM_EINVAL, "two-step plan does not fit");
+    RET(tb_alloc(c, s));
+    CUtensorMap tm[5];
+    RET(encode_3d(&tm[0], s.buf[parity], c->nx, c->ny, (int)s.buf_planes(), tv.TX + 16, tv.TY + 10));
+    RET(encode_3d(&tm[1], s.buf[parity ^ 1], c->nx, c->ny, (int)s.buf_planes(), tv.TX, tv.TY));
+    RET(encode_3d(&tm[2], s.C, c->nx, c->ny, s.nzl, tv.TX, tv.TY));
+    RET(encode_3d(&tm[3], s.alt[parity ^ 1], c->nx, c->ny, (int)s.buf_planes(), tv.TX + 16, tv.TY + 10));
+    RET(encode_3d(&tm[4], s.buf[parity], c->nx, c->ny, (int)s.buf_planes(), tv.TX, tv.TY));
+    TBParams p;
+    std::memset(&p, 0, sizeof p);
+    p.nx = c->nx;
+    p.ny = c->ny;
+    p.nzl = s.nzl;
+    p.plane = (long long)c->nx * c->ny;
+    p.coef[0] = 3.0f * c->coeffs[0];
+    for (int k = 1; k < 6; ++k) p.coef[k] = c->coeffs[k];
+    p.outA = s.alt[parity ^ 1];
+    p.outB = s.alt[parity];
+    p.d_step = s.d_step;
+    p.parity = parity;
+    p.flags = s.d_flags;
+    p.d_epoch = s.d_epoch;
+    p.nbands = (int)bands.size();
+    p.tiles_x = tiles_x;
+    p.nsrc = (int)s.srcs.size();
+    for (int k = 0; k < p.nsrc; ++k) p.src[k] = s.srcs[k];
+    p.samples = s.d_samples;
+    for (size_t b = 0; b < bands.size(); ++b) {
+        p.band = (int)b;
+        p.tiles_y = bands[b].tiles_y;
+        p.ya_lo = bands[b].ya_lo;
+        p.ya_hi = bands[b].ya_hi;
+        p.yb_lo = bands[b].yb_lo;
+        p.yb_hi = bands[b].yb_hi;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (c->profiling) {
+            const size_t k = 2 * (size_t)c->prof_launches;
+            while (c->prof_ev.size() < k + 2) {
+                cudaEvent_t e;
+                CK(cudaEventCreate(&e));
+                c->prof_ev.push_back(e);
+            }
+            e0 = c->prof_ev[k];
+            e1 = c->prof_ev[k + 1];
+            CK(cudaEventRecord(e0, st));
+        }
+        CK(launch_tb2(var, tm, p, st));
+        if (c->profiling) {
+            CK(cudaEventRecord(e1, st));
+            ++c->prof_launches;
+        }
+        ++c->launches;
+    }
+    CK(launch_tb_advance(s.d_step, parity, s.d_epoch, st));
+    ++c->launches;
+    std::swap(s.buf[0], s.alt[0]);
+    std::swap(s.buf[1], s.alt[1]);
+    s.bank ^= 1;
+    s.tm_variant = -1;  // k_stream tensor maps follow the buffers
+    return RTM_OK;
+}
+
+// A graph of 2*GRAPH_PAIRS passes (4*GRAPH_PAIRS steps): an even number of bank swaps, so it
+// starts and ends on the same bank; one graph per (bank, parity) it starts from.
+int tb_graph_launch(rtm_ctx* c, Slab& s, int parity, cudaStream_t st) {
+    const int var = resolve_tile(c);
+    const int key = s.bank * 2 + parity;
+    if (s.tb_graph_variant[key] != var) {
+        if (s.tb_graph[key]) cudaGraphExecDestroy(s.tb_graph[key]), s.tb_graph[key] = nullptr;
+        RET(tb_alloc(c, s));
+        CK(cudaStreamBeginCapture(s.s_own, cudaStreamCaptureModeThreadLocal));
+        const long long saved = c->launches;
+        int rc = RTM_OK;
+        for (int k = 0; k < 2 * GRAPH_PAIRS && rc == RTM_OK; ++k) rc = tb_pass(c, s, parity, s.s_own);
+        cudaGraph_t g = nullptr;
+        cudaError_t e = cudaStreamEndCapture(s.s_own, &g);
+        c->launches = saved;
+        if (rc != RTM_OK) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        if (e != cudaSuccess) return fail(RTM_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
+        cudaError_t ei = cudaGraphInstantiate(&s.tb_graph[key], g, 0);
+        cudaGraphDestroy(g);
+        if (ei != cudaSuccess) return fail(RTM_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(ei));
+        s.tb_graph_variant[key] = var;
+    }
+    CK(cudaGraphLaunch(s.tb_graph[key], st));
+    return RTM_OK;
 }
 
 int upload_sources(rtm_ctx* c, Slab& s) {
@@ -484,8 +672,27 @@ int step_single(rtm_ctx* c, int nsteps) {
     Slab& s = c->slabs[0];
     cudaStream_t st = s.stream();
     int k = 0;
+    int tb_bands = 0;
+    if (variant(resolve_tile(c)).kind == 3) {
+        int tx;
+        std::vector<TBBand> b;
+        if (tb_plan(c, variant(resolve_tile(c)), &tx, &b)) tb_bands = (int)b.size();
+    }
+    const bool tb = tb_bands > 0;
     while (k < nsteps) {
         const int parity = (int)(c->step & 1);
+        if (tb && nsteps - k >= 2) {  // two time steps per pass
+            const int passes = c->graphs && !c->profiling && nsteps - k >= 4 * GRAPH_PAIRS ? 2 * GRAPH_PAIRS : 1;
+            if (passes > 1) {
+                RET(tb_graph_launch(c, s, parity, st));
+                c->launches += (long long)passes * (tb_bands + 1);  // + d_step/epoch advance
+            } else {
+                RET(tb_pass(c, s, parity, st));
+            }
+            c->step += 2 * passes;
+            k += 2 * passes;
+            continue;
+        }
         if (c->graphs && !c->profiling && parity == 0 && nsteps - k >= 2 * GRAPH_PAIRS) {
             RET(build_graph(c, s));
             CK(cudaGraphLaunch(s.graph, st));
@@ -1097,6 +1304,7 @@ int rtm_set_step_count(rtm_ctx* c, long long n) {
             std::swap(s.buf[0], s.buf[1]);
             s.tm_variant = -1;  // tensor maps follow the buffers
             s.graph_valid = false;
+            for (int k = 0; k < 4; ++k) s.tb_graph_variant[k] = -1;
         }
     for (auto& s : c->slabs) {
         CK(cudaSetDevice(s.dev));
@@ -1173,6 +1381,10 @@ int rtm_set_option(rtm_ctx* c, int key, long long value) {
             if (value < 0 || value > (1 << 30)) return fail(RTM_EINVAL, "check interval %lld", value);
             c->check_every = (int)value;
             break;
+        case RTM_OPT_TB_CTAS:
+            if (value < 0 || value > (1 << 20)) return fail(RTM_EINVAL, "tb ctas %lld out of range", value);
+            c->tb_ctas = (int)value;
+            break;
         case RTM_OPT_HALO_MODE:
             if (value < 0 || value > 1) return fail(RTM_EINVAL, "halo mode %lld not in 0..1", value);
             if (value == 1 && c->mode != 1)
@@ -1211,6 +1423,7 @@ long long rtm_get_option(rtm_ctx* c, int key) {
         case RTM_OPT_SHOT_ORDER: return c->shot_order;
         case RTM_OPT_HALO_MODE: return c->halo_mode;
         case RTM_OPT_CHECK_EVERY: return c->check_every;
+        case RTM_OPT_TB_CTAS: return c->tb_ctas;
         default: return -1;
     }
 }

@@ -19,130 +19,12 @@
 // (b_i, b_j, b_k) blocksize) by an xy tile streamed along z; see DESIGN.md §Kernels.
 // =====================================================================================
 #include "rtm_internal.h"
+#include "rtm_device.cuh"
 
 #include <cstdio>
 #include <type_traits>
 
 namespace rtm {
-
-// ------------------------------------------------------------------------------------
-// The per-point update.  z[k], y[k], x[k] are u at offsets k-5 along each axis (index 5 is
-// the point itself, shared by all three).  ONE expression for every kernel, so all
-// variants are bitwise identical.  Order: centre * 3c0, then z, y, x pairs from the
-// nearest to the farthest offset, then the leapfrog.
-__device__ __forceinline__ float rtm_point(const float (&z)[11], const float (&y)[11],
-                                           const float (&x)[11], float up, float C,
-                                           const float (&c)[6]) {
-    float acc = __fmul_rn(c[0], z[5]);
-#pragma unroll
-    for (int m = 1; m <= 5; ++m) acc = __fmaf_rn(c[m], __fadd_rn(z[5 - m], z[5 + m]), acc);
-#pragma unroll
-    for (int m = 1; m <= 5; ++m) acc = __fmaf_rn(c[m], __fadd_rn(y[5 - m], y[5 + m]), acc);
-#pragma unroll
-    for (int m = 1; m <= 5; ++m) acc = __fmaf_rn(c[m], __fadd_rn(x[5 - m], x[5 + m]), acc);
-    return __fmaf_rn(C, acc, __fmaf_rn(2.0f, z[5], -up));
-}
-
-// The same expression for two x-adjacent points at once with Blackwell's packed fp32x2
-// instructions (FFMA2/FADD2/FMUL2: one issue slot for two lanes).  Each lane performs exactly
-// rtm_point's IEEE operations in rtm_point's order, so results are bitwise identical.  The x
-// pair sums c_m * (x[-m] + x[+m]) are passed in precomputed (xsum[m-1]).
-__device__ __forceinline__ float2 rtm_point2(const float2 (&z)[11], const float2 (&y)[11],
-                                             const float2 (&xsum)[5], float2 up, float2 C,
-                                             const float (&c)[6]) {
-    float2 acc = __fmul2_rn(make_float2(c[0], c[0]), z[5]);
-#pragma unroll
-    for (int m = 1; m <= 5; ++m)
-        acc = __ffma2_rn(make_float2(c[m], c[m]), __fadd2_rn(z[5 - m], z[5 + m]), acc);
-#pragma unroll
-    for (int m = 1; m <= 5; ++m)
-        acc = __ffma2_rn(make_float2(c[m], c[m]), __fadd2_rn(y[5 - m], y[5 + m]), acc);
-#pragma unroll
-    for (int m = 1; m <= 5; ++m) acc = __ffma2_rn(make_float2(c[m], c[m]), xsum[m - 1], acc);
-    const float2 lf = __ffma2_rn(make_float2(2.0f, 2.0f), z[5], make_float2(-up.x, -up.y));
-    return __ffma2_rn(C, acc, lf);
-}
-__device__ __forceinline__ float2 lo2(const float4& v) { return make_float2(v.x, v.y); }
-__device__ __forceinline__ float2 hi2(const float4& v) { return make_float2(v.z, v.w); }
-
-// ------------------------------------------------------------------------------------
-// PTX helpers: mbarrier + TMA
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-                 : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    while (!mbar_try_wait(bar, parity)) {
-    }
-}
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int x, int y, int z,
-                                            uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ float4 ld_stream4(const float* p) {  // read-once stream, evict-first
-    return __ldcs(reinterpret_cast<const float4*>(p));
-}
-__device__ __forceinline__ void st_stream4(float* p, float4 v) {
-    __stcs(reinterpret_cast<float4*>(p), v);
-}
-__device__ __forceinline__ float comp(const float4& v, int i) {
-    return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
-}
-
-// Fused halo push: mirror a finished boundary-plane value into the neighbour slab's z-halo.
-__device__ __forceinline__ void push_halo4(const StencilParams& p, int z, long long col, float4 v) {
-    if (z < 5 && p.push_lo) st_stream4(p.push_lo + (long long)z * p.plane + col, v);
-    if (z >= p.nzl - 5 && p.push_hi) st_stream4(p.push_hi + (long long)(z - p.nzl + 5) * p.plane + col, v);
-}
-
-// Add the samples of the sources owned by this thread's 4-point column at plane z.
-__device__ __forceinline__ void add_sources(const StencilParams& p, uint64_t mask, int x, int z,
-                                            float (&out)[4]) {
-    while (mask) {
-        const int s = __ffsll(static_cast<long long>(mask)) - 1;
-        mask &= mask - 1;
-        const DevSource& src = p.src[s];
-        if (src.z == z) {
-            const int n = *reinterpret_cast<volatile const int*>(&p.d_step[p.parity]);
-            if (n < src.nsamples) {
-                const float w = p.samples[src.offset + n];
-                const int i = src.x - x;
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (k == i) out[k] = __fadd_rn(out[k], w);
-            }
-        }
-    }
-}
 
 // ------------------------------------------------------------------------------------
 template <int TX, int TY, int K>
@@ -414,33 +296,6 @@ __global__ void __launch_bounds__(256) k_velocity(const float* v, float* C, long
 // unit boundaries.  Work units are (z-chunk, tile) pairs, chunk-major, dealt round-robin
 // to the persistent CTAs (unit = blockIdx.x + k * gridDim.x) so co-running CTAs are xy
 // neighbours at similar z.
-__device__ __forceinline__ void mbar_wait_u32(uint32_t addr, uint32_t parity) {
-    uint32_t ok;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(addr), "r"(parity)
-            : "memory");
-    } while (!ok);
-}
-__device__ __forceinline__ void mbar_arrive_u32(uint32_t addr) {
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
-}
-// Run f(integral_constant<O>), f(<O+1>), ... f(<U-1>) while iterations remain; false when the
-// unit ended inside the unrolled group.
-template <int O, int U, class F>
-__device__ __forceinline__ bool unrolled(F& f, int i, int n) {
-    f(std::integral_constant<int, O>{});
-    if constexpr (O + 1 < U) {
-        if (i + O + 1 >= n) return false;
-        return unrolled<O + 1, U>(f, i, n);
-    }
-    return true;
-}
-
 template <int TX, int TY, int K, int D>
 struct StreamShape {
     static constexpr int NW = TX * TY / 128;      // consumer warps (4 points per thread)
@@ -458,48 +313,6 @@ struct StreamShape {
     static_assert(K >= 7, "6 live planes + 1 in flight");
     static_assert(TX % 4 == 0 && RS <= 256 && ROWS <= 256 && TX <= 256 && TY <= 256, "TMA box");
 };
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-// cache_mode (StencilParams): bits 0-1 L2 prefetch of u_prev/C (0 none, 1 evict_last,
-// 2 evict_normal); bit 2 u TMA loads with an evict_last L2 policy; bit 3 plain (not
-// evict-first) u_prev/C loads and u_next stores; bits 4-7 prefetch distance in planes;
-// bits 8-9 L2 promotion of the u box (host side); bit 10 u_prev/C TMA loads evict_first.
-__device__ __forceinline__ void prefetch_l2(const void* p, int mode) {
-    if (mode == 1)
-        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
-    else if (mode == 2)
-        asm volatile("prefetch.global.L2::evict_normal [%0];" ::"l"(p));
-}
-__device__ __forceinline__ float4 ld_mode4(const float* p, bool plain) {
-    return plain ? __ldcg(reinterpret_cast<const float4*>(p)) : ld_stream4(p);
-}
-__device__ __forceinline__ void st_mode4(float* p, float4 v, bool plain) {
-    if (plain)
-        __stcg(reinterpret_cast<float4*>(p), v);
-    else
-        st_stream4(p, v);
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* tm, int x, int y,
-                                                 int z, uint64_t* bar, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(pol)
-        : "memory");
-}
 
 struct UnitGeom {
     int x0, y0, zs, ze;
@@ -820,9 +633,12 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
     X(36, "stream64x28k10d6u11", 2, 64, 28, 10, 6, 1, 11)
 
 static const TileVariant kVariants[] = {
-    {"naive", 0, 0, 0, 0, 0, 0, 1},
-#define X(id, name, kind, tx, ty, k, d, mb, u) {name, kind, tx, ty, k, d, mb, u},
+    {"naive", 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0},
+#define X(id, name, kind, tx, ty, k, d, mb, u) {name, kind, tx, ty, k, d, mb, u, 0, 0, 0, 0},
     RTM_VARIANTS(X)
+#undef X
+#define X(id, name, tx, ty, ka, kb, da, db, l, u, pair) {name, 3, tx, ty, ka, da, 1, u, kb, db, l, pair},
+    RTM_TB_VARIANTS(X)
 #undef X
 };
 
@@ -847,6 +663,7 @@ static cudaError_t prepare(const void** fn, int* threads, size_t* smem) {
 }
 
 static cudaError_t variant_fn(int id, const void** fn, int* threads, size_t* smem) {
+    if (id > 0 && id < num_variants() && variant(id).kind == 3) return tb_variant_fn(id, fn, threads, smem);
     switch (id) {
 #define X(vid, name, kind, tx, ty, k, d, mb, u) \
     case vid:                                   \
@@ -884,6 +701,7 @@ cudaError_t launch_variant(int id, const CUtensorMap* tm_u, const CUtensorMap* t
     const void* fn;
     int threads;
     size_t smem;
+    if (variant(id).kind == 3) return cudaErrorInvalidValue;  // two-step passes: launch_tb2
     cudaError_t e = variant_fn(id, &fn, &threads, &smem);
     if (e != cudaSuccess) return e;
     const long long units = (long long)p.tiles_x * p.tiles_y *

@@ -580,3 +580,102 @@ def test_field_stats_and_instability_detection(P):
             sim.step(5)
         assert e.value.code == P.RTM_EUNSTABLE
         assert sim.steps_taken == 3  # stopped at the first check
+
+
+# ----------------------------------------------------------------------------- two-step passes (f4)
+def _tb_ids(P):
+    return [t for t in range(P.rtm_num_tiles()) if P.rtm_tile_name(t).startswith("tb2_")]
+
+
+def _run_opts(P, v, steps, u0, up0, src, tile, tb_ctas=0, graphs=1, chunks=None):
+    nz, ny, nx = v.shape
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32) as sim:
+        sim.set_tile(tile)
+        P.rtm_set_option(sim.h, P.RTM_OPT_TB_CTAS, tb_ctas)
+        P.rtm_set_option(sim.h, P.RTM_OPT_GRAPHS, graphs)
+        sim.set_velocity(v)
+        for s in src:
+            sim.inject_source(*s)
+        sim.set_fields(u0, up0)
+        for k in (chunks or [steps]):
+            sim.step(k)
+        return sim.read_fields()
+
+
+@pytest.mark.parametrize("tb_ctas", [0, 12, 24])
+def test_tb2_bitwise_equals_single_step(P, tb_ctas):
+    """Two steps per pass (k_tb2) give exactly the bits of two single steps (k_stream): same
+    per-point expression, u^{n+1} handed between CTAs through L2.  tb_ctas = 12 / 24 force
+    multi-band plans (redundant A rows at every band edge) on a ragged 200 x 150 plane;
+    sources sit on band edges, on the z ends and in the ragged x tail."""
+    nz, ny, nx = 23, 150, 200
+    rng = np.random.default_rng(77)
+    v = rng.uniform(1500, 4300, (nz, ny, nx)).astype(np.float32)
+    u0, up0 = ri.random_fields(v.shape, seed=77)
+    w = ri.source_samples(3000.0, 1e-3, 15.0, 9)
+    src = [(5, 0, 0, w), (199, 149, 22, -w), (130, 36, 11, w), (64, 37, 3, 0.5 * w),
+           (63, 38, 19, w), (100, 75, 12, w), (196, 112, 7, -w), (17, 113, 7, w)]
+    ref_u, ref_up = _run_opts(P, v, 9, u0, up0, src, 35)
+    for t in _tb_ids(P):
+        u, up = _run_opts(P, v, 9, u0, up0, src, t, tb_ctas=tb_ctas)
+        assert np.array_equal(u, ref_u), P.rtm_tile_name(t)
+        assert np.array_equal(up, ref_up), P.rtm_tile_name(t)
+
+
+def test_tb2_graphs_odd_starts_and_short_z(P):
+    """Graph replays of 16 passes (from both parities and both buffer banks), odd remainders
+    and direct passes all agree bitwise with single steps; nz smaller than the lag."""
+    for shape in [(70, 40, 64), (3, 33, 48), (1, 20, 32)]:
+        nz, ny, nx = shape
+        rng = np.random.default_rng(nz)
+        v = rng.uniform(1500, 4300, shape).astype(np.float32)
+        u0, up0 = ri.random_fields(shape, seed=nz)
+        w = ri.source_samples(3000.0, 1e-3, 15.0, 80)
+        src = [(nx // 2, ny // 2, nz // 2, w)]
+        ref_u, _ = _run_opts(P, v, 75, u0, up0, src, 35, chunks=[75])
+        tb = _tb_ids(P)[0]
+        for chunks in ([75], [1, 33, 1, 40], [2, 2, 32, 39]):
+            u, _ = _run_opts(P, v, 75, u0, up0, src, tb, chunks=chunks)
+            assert np.array_equal(u, ref_u), (shape, chunks)
+        u, _ = _run_opts(P, v, 75, u0, up0, src, tb, graphs=0, tb_ctas=6)
+        assert np.array_equal(u, ref_u), shape
+
+
+def test_tb2_c1_c2_full_runs_vs_oracle(P):
+    """The configs' full step counts through the two-step path vs the fp32 oracle
+    (north_star tolerance 1e-4 max|u|)."""
+    tb = _tb_ids(P)[0]
+    for k in (1, 2):
+        cfg = ri.make_config(k)
+        v = cfg.velocity()
+        src = cfg.sources()
+        ref = oracle.run(v, cfg.dx, cfg.dt, C32, cfg.steps, sources=src)
+        got = gpu_run(P, v, cfg.dx, cfg.dt, cfg.steps, sources=src, tile=tb)
+        assert relerr(got, ref) <= TOL_FULL, k
+
+
+def test_full_size_c4_tb2_sampled(P):
+    """C4 (1024^3, 8 y-bands) two steps through k_tb2 from random ICs: bitwise equal to two
+    single steps of k_stream (itself sampled against the oracle at this size), and u^1 —
+    produced by stage A and consumed by stage B through L2 — sampled against the oracle."""
+    cfg = ri.make_config(4)
+    v = cfg.velocity()
+    u0, up0 = ri.random_fields(v.shape, seed=45)
+    tb = _tb_ids(P)[0]
+    outs = {}
+    for t in (35, tb):
+        with P.Simulation(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, C32) as sim:
+            sim.set_tile(t)
+            sim.set_velocity(v)
+            sim.set_fields(u0, up0)
+            sim.step(2)
+            outs[t] = sim.read_fields()
+    assert np.array_equal(outs[tb][0], outs[35][0])
+    assert np.array_equal(outs[tb][1], outs[35][1])
+    u1 = outs[tb][1]  # u^1
+    rng = np.random.default_rng(405)
+    nz, ny, nx = v.shape
+    pts = np.stack([rng.integers(0, nx, 50_000), rng.integers(0, ny, 50_000),
+                    rng.integers(0, nz, 50_000)], 1).astype(np.int32)
+    ref1 = oracle.points_f32(v, cfg.dx, cfg.dt, C32, u0, up0, pts)
+    assert relerr(u1[pts[:, 2], pts[:, 1], pts[:, 0]], ref1) <= TOL_1
