@@ -29,7 +29,7 @@ sys.path.insert(0, str(ROOT))
 import numpy as np  # noqa: E402
 
 BYTES_PER_POINT = 16  # compulsory fp32 traffic per point update: read u, u_prev, C; write u_next
-# two-step passes (k_tb2): read u^n, u^{n-1}, C; write u^{n+1}, u^{n+2}
+# two-step passes (k_tb2s): read u^n, u^{n-1}, C; write u^{n+1}, u^{n+2}
 # = 20 B per two point updates
 BYTES_PER_POINT_TB2 = 10
 METRIC = "stencil Gpoints/s and achieved HBM GB/s (% of ~8 TB/s) at 1/2/4/8 B200"
@@ -261,7 +261,7 @@ def main():
         # stream-kernel variant timed on this grid (max over ranks = MWMB), winner verified
         P.rtm_set_velocity_device(h, d_v.data_ptr())
         cands = [t for t in range(P.rtm_num_tiles())
-                 if (P.rtm_tile_name(t) or "").startswith(("stream", "tb2_"))]
+                 if (P.rtm_tile_name(t) or "").startswith(("stream", "tb2"))]
         res, times = P.rtm_autotune(h, args.tune_ni, tiles=cands)
         tune = {"selected": P.rtm_tile_name(res["best_tile"]), "candidates": len(cands),
                 "nI": args.tune_ni, "min_time_ms": round(res["min_time_ms"], 4),
@@ -329,7 +329,7 @@ def main():
     # batched shots share C: 12 B/pt for u, u_prev, u_next + 4 B/pt of C per shot batch
     bytes_per_pt = BYTES_PER_POINT if shots == 1 else 12.0 + 4.0 / shots
     tile_name = P.rtm_tile_name(P.rtm_get_tile(h))
-    two_step = tile_name.startswith("tb2_") and shots == 1 and world == 1 and nsteps >= 2
+    two_step = tile_name.startswith("tb2") and shots == 1 and world == 1 and nsteps >= 2
     if two_step:  # every launch is a two-step band pass (odd remainders: one k_stream step)
         bytes_per_pt = BYTES_PER_POINT_TB2
     alg_bytes = bytes_per_pt * pts_local * nsteps * args.steps
@@ -386,8 +386,8 @@ def main():
                          "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4) if achieved else None,
                          "traffic": traffic, "peak_source": peak_src,
-                         "kernel": ("k_tb2" if two_step else
-                                    "k_stream" if tile_name.startswith(("stream", "tb2_")) else
+                         "kernel": ("k_tb2s" if two_step else
+                                    "k_stream" if tile_name.startswith(("stream", "tb2")) else
                                     "k_tiled" if tile_name.startswith("tma") else "k_naive")
                                    + f"<{tile_name}>", "launches": kl,
                          "measured": roof_src,

@@ -99,7 +99,7 @@ struct Slab {
     int graph_variant = -1;
     int graph_bank = 0;
     bool graph_valid = false;
-    // two-step passes (kind 3): the second bank they write, then the banks swap
+    // two-step passes (kind 4): the second bank they write, then the banks swap
     float* alt[2] = {nullptr, nullptr};
     int bank = 0;                              // toggled at every bank swap
     unsigned long long* d_flags = nullptr;     // stage-A progress per CTA of a band
@@ -306,11 +306,11 @@ int resolve_tile(const rtm_ctx* c) {
     return 35;  // stream64x30k10d6u4: best on C4 (profiles/sweep_c4_s6.log); bench autotunes
 }
 
-// The variant that runs single time steps: a two-step variant (kind 3) runs its paired
+// The variant that runs single time steps: a two-step variant (kind 4) runs its paired
 // k_stream variant for odd remainders and for contexts it does not cover (slabs, shots).
 int single_variant(const rtm_ctx* c) {
     const int v = resolve_tile(c);
-    return variant(v).kind == 3 ? variant(v).pair : v;
+    return variant(v).kind >= 3 ? variant(v).pair : v;
 }
 
 int encode_3d(CUtensorMap* tm, void* base, int nx, int ny, int nplanes, int bx, int by,
@@ -490,7 +490,25 @@ void invalidate_graphs(rtm_ctx* c) {
     }
 }
 
-// ---- two-step passes (kind 3, k_tb2 in rtm_tb.cu) ----------------------
+// ---- two-step passes (kind 4, k_tb2s in rtm_tb.cu) ----------------------
+// CUDA events around a launch when profiling (rtm_set_profiling)
+int prof_begin(rtm_ctx* c, cudaStream_t st) {
+    if (!c->profiling) return RTM_OK;
+    const size_t k = 2 * (size_t)c->prof_launches;
+    while (c->prof_ev.size() < k + 2) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        c->prof_ev.push_back(e);
+    }
+    CK(cudaEventRecord(c->prof_ev[k], st));
+    return RTM_OK;
+}
+int prof_end(rtm_ctx* c, cudaStream_t st) {
+    if (!c->profiling) return RTM_OK;
+    CK(cudaEventRecord(c->prof_ev[2 * (size_t)c->prof_launches + 1], st));
+    ++c->prof_launches;
+    return RTM_OK;
+}
 struct TBBand {
     int ya_lo, ya_hi, yb_lo, yb_hi, tiles_y;
 };
@@ -527,7 +545,7 @@ bool tb_plan(const rtm_ctx* c, const TileVariant& tv, int* tiles_x, std::vector<
 
 bool tb_active(const rtm_ctx* c) {
     const int v = resolve_tile(c);
-    if (variant(v).kind != 3) return false;
+    if (variant(v).kind < 3) return false;
     int tx;
     std::vector<TBBand> b;
     return tb_plan(c, variant(v), &tx, &b);
@@ -545,9 +563,9 @@ int tb_alloc(rtm_ctx* c, Slab& s) {
         }
         CK(cudaMemsetAsync(s.alt[b], 0, nbuf * sizeof(float), s.stream()));  // z-halo planes stay 0
     }
-    CK(cudaMalloc(&s.d_flags, (size_t)c->num_sms * sizeof(unsigned long long)));
+    CK(cudaMalloc(&s.d_flags, 2 * (size_t)c->num_sms * sizeof(unsigned long long)));
     CK(cudaMalloc(&s.d_epoch, sizeof(unsigned long long)));
-    CK(cudaMemsetAsync(s.d_flags, 0, (size_t)c->num_sms * sizeof(unsigned long long), s.stream()));
+    CK(cudaMemsetAsync(s.d_flags, 0, 2 * (size_t)c->num_sms * sizeof(unsigned long long), s.stream()));
     CK(cudaMemsetAsync(s.d_epoch, 0, sizeof(unsigned long long), s.stream()));
     CK(cudaStreamSynchronize(s.stream()));
     return RTM_OK;
@@ -563,55 +581,44 @@ int tb_pass(rtm_ctx* c, Slab& s, int parity, cudaStream_t st) {
     std::vector<TBBand> bands;
     if (!tb_plan(c, tv, &tiles_x, &bands)) return fail(RTM_EINVAL, "two-step plan does not fit");
     RET(tb_alloc(c, s));
-    CUtensorMap tm[5];
-    RET(encode_3d(&tm[0], s.buf[parity], c->nx, c->ny, (int)s.buf_planes(), tv.TX + 16, tv.TY + 10));
-    RET(encode_3d(&tm[1], s.buf[parity ^ 1], c->nx, c->ny, (int)s.buf_planes(), tv.TX, tv.TY));
-    RET(encode_3d(&tm[2], s.C, c->nx, c->ny, s.nzl, tv.TX, tv.TY));
-    RET(encode_3d(&tm[3], s.alt[parity ^ 1], c->nx, c->ny, (int)s.buf_planes(), tv.TX + 16, tv.TY + 10));
-    RET(encode_3d(&tm[4], s.buf[parity], c->nx, c->ny, (int)s.buf_planes(), tv.TX, tv.TY));
-    TBParams p;
-    std::memset(&p, 0, sizeof p);
-    p.nx = c->nx;
-    p.ny = c->ny;
-    p.nzl = s.nzl;
-    p.plane = (long long)c->nx * c->ny;
-    p.coef[0] = 3.0f * c->coeffs[0];
-    for (int k = 1; k < 6; ++k) p.coef[k] = c->coeffs[k];
-    p.outA = s.alt[parity ^ 1];
-    p.outB = s.alt[parity];
-    p.d_step = s.d_step;
-    p.parity = parity;
-    p.flags = s.d_flags;
-    p.d_epoch = s.d_epoch;
-    p.nbands = (int)bands.size();
-    p.tiles_x = tiles_x;
-    p.nsrc = (int)s.srcs.size();
-    for (int k = 0; k < p.nsrc; ++k) p.src[k] = s.srcs[k];
-    p.samples = s.d_samples;
+    CUtensorMap tm[6];
+    const int np = (int)s.buf_planes();
+    RET(encode_3d(&tm[0], s.buf[parity], c->nx, c->ny, np, tv.TX + 16, tv.TY + 10));  // u^n box
+    RET(encode_3d(&tm[1], s.buf[parity ^ 1], c->nx, c->ny, np, tv.TX, tv.TY));        // u^{n-1}
+    RET(encode_3d(&tm[2], s.C, c->nx, c->ny, s.nzl, tv.TX, tv.TY));                   // C
+    RET(encode_3d(&tm[3], s.alt[parity ^ 1], c->nx, c->ny, np, tv.TX + 16, tv.TY + 10));  // u^{n+1} box
+    RET(encode_3d(&tm[4], s.buf[parity], c->nx, c->ny, np, tv.TX, tv.TY));            // u^n tile
+    RET(encode_3d(&tm[5], s.alt[parity ^ 1], c->nx, c->ny, np, tv.TX, tv.TY));        // u^{n+1} store
+    TB2SParams q;
+    std::memset(&q, 0, sizeof q);
+    q.nx = c->nx;
+    q.ny = c->ny;
+    q.nzl = s.nzl;
+    q.plane = (long long)c->nx * c->ny;
+    q.coef[0] = 3.0f * c->coeffs[0];
+    for (int k = 1; k < 6; ++k) q.coef[k] = c->coeffs[k];
+    q.outB = s.alt[parity];
+    q.d_step = s.d_step;
+    q.parity = parity;
+    q.flagsA = s.d_flags;
+    q.flagsB = s.d_flags + c->num_sms;
+    q.d_epoch = s.d_epoch;
+    q.nbands = (int)bands.size();
+    q.tiles_x = tiles_x;
+    q.nsrc = (int)s.srcs.size();
+    for (int k = 0; k < q.nsrc; ++k) q.src[k] = s.srcs[k];
+    q.samples = s.d_samples;
     for (size_t b = 0; b < bands.size(); ++b) {
-        p.band = (int)b;
-        p.tiles_y = bands[b].tiles_y;
-        p.ya_lo = bands[b].ya_lo;
-        p.ya_hi = bands[b].ya_hi;
-        p.yb_lo = bands[b].yb_lo;
-        p.yb_hi = bands[b].yb_hi;
-        cudaEvent_t e0 = nullptr, e1 = nullptr;
-        if (c->profiling) {
-            const size_t k = 2 * (size_t)c->prof_launches;
-            while (c->prof_ev.size() < k + 2) {
-                cudaEvent_t e;
-                CK(cudaEventCreate(&e));
-                c->prof_ev.push_back(e);
-            }
-            e0 = c->prof_ev[k];
-            e1 = c->prof_ev[k + 1];
-            CK(cudaEventRecord(e0, st));
-        }
-        CK(launch_tb2(var, tm, p, st));
-        if (c->profiling) {
-            CK(cudaEventRecord(e1, st));
-            ++c->prof_launches;
-        }
+        q.band = (int)b;
+        q.tiles_y = bands[b].tiles_y;
+        q.ntiles = tiles_x * bands[b].tiles_y;
+        q.ya_lo = bands[b].ya_lo;
+        q.ya_hi = bands[b].ya_hi;
+        q.yb_lo = bands[b].yb_lo;
+        q.yb_hi = bands[b].yb_hi;
+        RET(prof_begin(c, st));
+        CK(launch_tb2s(var, tm, q, st));
+        RET(prof_end(c, st));
         ++c->launches;
     }
     CK(launch_tb_advance(s.d_step, parity, s.d_epoch, st));
@@ -673,7 +680,7 @@ int step_single(rtm_ctx* c, int nsteps) {
     cudaStream_t st = s.stream();
     int k = 0;
     int tb_bands = 0;
-    if (variant(resolve_tile(c)).kind == 3) {
+    if (variant(resolve_tile(c)).kind >= 3) {
         int tx;
         std::vector<TBBand> b;
         if (tb_plan(c, variant(resolve_tile(c)), &tx, &b)) tb_bands = (int)b.size();

@@ -51,45 +51,20 @@ struct StencilParams {
 struct TileVariant {
     const char* name;
     int kind;                  // 0 naive, 1 k_tiled (CTA per unit), 2 k_stream (persistent, producer
-                               // warp), 3 k_tb2 (two time steps per HBM pass)
+                               // warp), 4 k_tb2s (two time steps per HBM pass)
     int TX, TY, K, D, MINB;    // tile (x, y), u ring depth, u_prev/C ring depth (0: LDG), min CTAs/SM
     int U;                     // z-loop unroll (register-queue rotation amortised over U planes)
-    int KB, DB, L;             // kind 3: second-step u ring / u^n,C ring depths, lag (planes)
-    int pair;                  // kind 3: the k_stream variant that runs single (odd) steps
+    int KB, DB, L;             // kind 4: KB = W (store groups in flight before publication),
+                               // DB = L2 hint bits, L = LMAX (stage-A lead bound, planes)
+    int pair;                  // kind 4: the k_stream variant that runs single (odd) steps
 };
 
-// Two-step temporal blocking (kind 3, k_tb2 in rtm_tb.cu).  One launch covers one y-band of a
-// single-slab, single-shot grid for two time steps n -> n+2: stage A computes u^{n+1} on the
-// band's rows plus 5 rows each side (A region) and stores it to outA; stage B computes u^{n+2}
-// on the band's own rows from u^{n+1} (read back through L2 as neighbouring CTAs publish their
-// planes) and stores it to outB.  All CTAs of a band are co-resident (cooperative launch) and
-// sweep z together; flags[] carry per-CTA stage-A progress (epoch << 32 | planes done).
-struct TBParams {
-    int nx, ny, nzl;
-    long long plane;
-    float coef[6];
-    float* outA;                        // u^{n+1} buffer base (nzl+10 planes), other bank
-    float* outB;                        // u^{n+2} buffer base, other bank
-    const int* d_step;                  // d_step[parity] = n
-    int parity;
-    unsigned long long* flags;          // [tiles_x * tiles_y] stage-A progress of each CTA
-    const unsigned long long* d_epoch;  // launch epoch (advanced once per pass)
-    int band, nbands;
-    int tiles_x, tiles_y;               // CTA grid of this band
-    int ya_lo, ya_hi;                   // stage-A rows [ya_lo, ya_hi)
-    int yb_lo, yb_hi;                   // stage-B rows [yb_lo, yb_hi)
-    int nsrc;
-    DevSource src[RTM_MAX_SOURCES];
-    const float* samples;
-};
 
-// Two-step (kind 3) variants, ids after the single-step table:
-//   X(id, name, TX, TY, KA, KB, DA, DB, L, U, pair)
-#define RTM_TB_VARIANTS(X)                                              \
-    X(37, "tb2_64x16a8b8d4l16u4", 64, 16, 8, 8, 4, 4, 16, 4, 35)       \
-    X(38, "tb2_64x16a8b8d3l24u4", 64, 16, 8, 8, 3, 3, 24, 4, 35)       \
-    X(39, "tb2_64x16a8b8d4l32u4", 64, 16, 8, 8, 4, 4, 32, 4, 35)       \
-    X(40, "tb2_64x14a8b8d4l24u4", 64, 14, 8, 8, 4, 4, 24, 4, 35)
+// Split-role two-step (kind 4) variants: X(id, name, TX, TY, K, D, U, LMAX, W, CH, pair)
+#define RTM_TB2S_VARIANTS(X)                                              \
+    X(37, "tb2s_64x16k8d3l24w6u4", 64, 16, 8, 3, 4, 24, 6, 0, 35)         \
+    X(38, "tb2s_64x16k8d3l40w6u4", 64, 16, 8, 3, 4, 40, 6, 0, 35)         \
+    X(39, "tb2s_64x16k8d3l56w16u4", 64, 16, 8, 3, 4, 56, 16, 0, 35)
 
 // Variant table: index 0 is the naive kernel.
 int num_variants();
@@ -106,13 +81,34 @@ cudaError_t launch_variant(int id, const CUtensorMap* tm_u, const CUtensorMap* t
                            cudaStream_t s);
 cudaError_t launch_naive(const StencilParams& p, cudaStream_t s);
 
-// kind 3: tm[0] u^n box (TX+16)x(TY+10), tm[1] u^{n-1} tile, tm[2] C tile, tm[3] u^{n+1} box,
-// tm[4] u^n tile.  Grid = p.tiles_x * p.tiles_y CTAs, launched cooperatively (co-resident).
-cudaError_t launch_tb2(int id, const CUtensorMap tm[5], const TBParams& p, cudaStream_t s);
+// Split-role two-step pass (kind 4, k_tb2s in rtm_tb.cu): stage-A and stage-B CTAs of each
+// tile (2 per SM); stage A publishes u^{n+1} planes through TMA stores (flagsA), stage B
+// reports progress (flagsB) that throttles stage A.
+struct TB2SParams {
+    int nx, ny, nzl;
+    long long plane;
+    float coef[6];
+    float* outB;                        // u^{n+2} (stage-B STG stores, band rows only)
+    const int* d_step;
+    int parity;
+    unsigned long long* flagsA;         // [ntiles] stage-A published planes
+    unsigned long long* flagsB;         // [ntiles] stage-B completed planes (throttle only)
+    const unsigned long long* d_epoch;
+    int band, nbands, ntiles;
+    int tiles_x, tiles_y;
+    int ya_lo, ya_hi, yb_lo, yb_hi;
+    int nsrc;
+    DevSource src[RTM_MAX_SOURCES];
+    const float* samples;
+};
+
+// kind 4: tm[0] u^n box (TX+16)x(TY+10), tm[1] u^{n-1} tile, tm[2] C tile, tm[3] u^{n+1} box,
+// tm[4] u^n tile, tm[5] u^{n+1} TX x TY box (TMA store).  Grid 2 * p.ntiles, cooperative.
+cudaError_t launch_tb2s(int id, const CUtensorMap tm[6], const TB2SParams& p, cudaStream_t s);
+cudaError_t tb2s_variant_fn(int id, const void** fn, int* threads, size_t* smem);
 // after the last band of a pass: d_step[parity] += 2, ++*d_epoch
 cudaError_t launch_tb_advance(int* d_step, int parity, unsigned long long* d_epoch, cudaStream_t s);
-// kind-3 kernel attributes (smem opt-in done); 0 on success
-cudaError_t tb_variant_fn(int id, const void** fn, int* threads, size_t* smem);
+cudaError_t tb2s_variant_fn(int id, const void** fn, int* threads, size_t* smem);
 
 // a1: C = fp32((double(v)*dt/dx)^2), stats[0] = max(v) bits (v > 0), stats[1] = count of
 // invalid (non-finite or <= 0) velocities.  v and C may alias.

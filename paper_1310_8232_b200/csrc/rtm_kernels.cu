@@ -637,8 +637,8 @@ static const TileVariant kVariants[] = {
 #define X(id, name, kind, tx, ty, k, d, mb, u) {name, kind, tx, ty, k, d, mb, u, 0, 0, 0, 0},
     RTM_VARIANTS(X)
 #undef X
-#define X(id, name, tx, ty, ka, kb, da, db, l, u, pair) {name, 3, tx, ty, ka, da, 1, u, kb, db, l, pair},
-    RTM_TB_VARIANTS(X)
+#define X(id, name, tx, ty, k, d, u, lmax, w, ch, pair) {name, 4, tx, ty, k, d, 2, u, w, ch, lmax, pair},
+    RTM_TB2S_VARIANTS(X)
 #undef X
 };
 
@@ -663,7 +663,7 @@ static cudaError_t prepare(const void** fn, int* threads, size_t* smem) {
 }
 
 static cudaError_t variant_fn(int id, const void** fn, int* threads, size_t* smem) {
-    if (id > 0 && id < num_variants() && variant(id).kind == 3) return tb_variant_fn(id, fn, threads, smem);
+    if (id > 0 && id < num_variants() && variant(id).kind == 4) return tb2s_variant_fn(id, fn, threads, smem);
     switch (id) {
 #define X(vid, name, kind, tx, ty, k, d, mb, u) \
     case vid:                                   \
@@ -701,7 +701,7 @@ cudaError_t launch_variant(int id, const CUtensorMap* tm_u, const CUtensorMap* t
     const void* fn;
     int threads;
     size_t smem;
-    if (variant(id).kind == 3) return cudaErrorInvalidValue;  // two-step passes: launch_tb2
+    if (variant(id).kind >= 3) return cudaErrorInvalidValue;  // two-step passes: launch_tb2s
     cudaError_t e = variant_fn(id, &fn, &threads, &smem);
     if (e != cudaSuccess) return e;
     const long long units = (long long)p.tiles_x * p.tiles_y *

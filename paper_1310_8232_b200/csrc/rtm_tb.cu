@@ -1,32 +1,31 @@
 // =====================================================================================
-// k_tb2: two time steps of the RTM 3D-model update (§2, Algorithm 1)
+// k_tb2s: two time steps of the RTM 3D-model update (§2, Algorithm 1)
 // per HBM pass — temporal blocking, SURVEY.md §8(f) f4 (§4 names time blocking
 // among the related stencil optimisations).
 //
 // The single-step kernel (k_stream) moves 16 B per point update and runs at the HBM copy
-// peak.  k_tb2 reads u^n, u^{n-1}, C once and writes u^{n+1}, u^{n+2}: 20 B per two updates.
-// The intermediate level u^{n+1} is consumed from L2 shortly after it is produced:
+// peak.  A two-step pass reads u^n, u^{n-1}, C once and writes u^{n+1}, u^{n+2}: 20 B per two
+// updates, with the intermediate level u^{n+1} produced and consumed through L2:
 //
-//   * The grid is cut into y-bands; one launch per band.  The band's CTAs (all co-resident,
-//     cooperative launch, one per SM) own fixed xy tiles of the band's A region = the band's
-//     rows plus 5 rows each side, and sweep z from 0 to nz together.
-//   * Stage A (step n -> n+1) on plane z: the k_stream algorithm (TMA ring of halo'd u^n
-//     planes, 11-plane register queue along z, packed FP32x2 point update), result stored to
-//     outA (L2-resident for now; it is also the next pass's u_prev).  Each consumer warp
-//     arrives (release.cta) on a per-plane mbarrier; a publisher warp waits for the CTA's
-//     completed planes and releases flags[cta] = epoch<<32 | planes done at gpu scope.
-//   * Stage B (step n+1 -> n+2) on plane z-L: a second producer warp waits (acquire) until
-//     this CTA and its four edge neighbours have published A through plane z-L+5, then TMAs
-//     the halo'd u^{n+1} box (from L2) into a second ring; the same consumer threads compute
-//     u^{n+2} on the band's own rows and stream it to outB.
-//   * Rows of the A region outside the band are recomputed by the neighbouring band
-//     (redundant work ~ 10 / band rows); both bands store bitwise-identical values.
-//
-// Every point is computed by star4() = the exact arithmetic of k_stream (rtm_device.cuh), so
-// k_tb2 results are bitwise identical to two k_stream steps (tests/test_gpu_parity.py).
-// Deadlock freedom: stage A never waits on other CTAs; stage B of plane j waits only for A
-// planes <= j+5 < the plane the slowest warp anywhere is working on (lag L >= 6), and all CTAs
-// are resident.  Every spin has a 4 s watchdog that traps (a launch error, never a hang).
+//   * The grid is cut into y-bands; one launch per band.  Each tile of the band's A region
+//     (the band's rows plus 5 rows each side) has a stage-A CTA (step n -> n+1) and a stage-B
+//     CTA (step n+1 -> n+2); all CTAs are co-resident (cooperative launch, 2 per SM) and sweep
+//     z from 0 to nz.  Rows of the A region outside the band are recomputed by the
+//     neighbouring band (redundant work ~ 10 / band rows); both store bitwise-identical values.
+//   * Both roles run k_stream's pipeline: a producer warp TMAs the halo'd u box and the
+//     (u_prev, C) tiles into rings; consumer warps keep an 11-plane register queue along z and
+//     compute star4() = k_stream's exact arithmetic, so results are bitwise identical to two
+//     k_stream steps (tests/test_gpu_parity.py).
+//   * Publication of u^{n+1} (stage A): consumers write each plane into a shared-memory
+//     staging slot; a store warp issues one TMA tensor store per plane (async proxy end to
+//     end) and, once the writes of plane i - W are complete (bulk wait_group), hands the plane
+//     to a publisher warp that releases flagsA[tile] = epoch << 32 | planes at gpu scope.
+//   * Stage-B producers acquire flagsA of their tile and its 4 edge neighbours (the box halo)
+//     before each u^{n+1} load; stage B reports its progress (flagsB) to throttle stage A to
+//     at most LMAX planes ahead, which bounds the L2 working set.
+// Deadlock freedom: a throttled stage-A CTA still drains and publishes every plane it has
+// loaded; stage B of plane j needs A planes <= j+5 < j + LMAX.  Every spin has a 4 s watchdog
+// that traps (a launch error, never a hang).
 // =====================================================================================
 #include "rtm_internal.h"
 #include "rtm_device.cuh"
@@ -77,9 +76,73 @@ __device__ __forceinline__ void mbar_wait_wd(uint32_t addr, uint32_t parity) {
     } while (!ok);
 }
 
-// Sources of this thread's 4-point column at plane z with sample index n (a3, fused).
-__device__ __forceinline__ void add_sources_n(const TBParams& p, uint64_t mask, int x, int z,
-                                              int n, float (&out)[4]) {
+// ====================================================================================
+// k_tb2s: the same two-step pass with the two stages on separate CTAs (2 per SM).  CTA
+// b < ntiles is the stage-A CTA of tile b, CTA ntiles + b the stage-B CTA of tile b; each is
+// a k_stream pipeline (producer warp, TMA rings, consumer warps with the z register queue).
+//   * Stage-A consumers write u^{n+1} into a shared-memory staging slot; a store warp issues
+//     one TMA tensor store per plane (async proxy end to end: no per-warp memory fences),
+//     and once bulk group i is complete publishes flagsA[tile] = E | (i+1) (proxy fence +
+//     gpu-scope release).
+//   * Stage-B producers acquire flagsA of the tile and its 4 edge neighbours before each TMA
+//     load of the halo'd u^{n+1} box; stage-B CTAs publish their progress (flagsB, relaxed)
+//     only to throttle stage A: A's producer keeps plane i within LMAX planes of B, which
+//     bounds the L2 working set (u^{n+1} window and the u^n/C re-reads of stage B).
+// Deadlock freedom: a throttled stage-A CTA still drains every plane it has loaded, so its
+// published count reaches the plane its producer waits at; stage B of plane j needs A planes
+// <= j+5 < j + LMAX (LMAX >= 7).  All CTAs are co-resident (cooperative launch).
+
+template <int TX, int TY, int K, int D, int S>
+struct TB2SShape {
+    static constexpr int NW = TX * TY / 128;
+    static constexpr int NT = (NW + 3) * 32;  // + producer, store warp, publisher warp
+    static constexpr int TXV = TX / 4;
+    static constexpr int RS = TX + 16;
+    static constexpr int ROWS = TY + 10;
+    static constexpr int USLOT = (RS * ROWS + 31) / 32 * 32;
+    static constexpr uint32_t UBYTES = RS * ROWS * 4;
+    static constexpr int CSLOT = 2 * TX * TY;
+    static constexpr uint32_t CBYTES = CSLOT * 4;
+    static constexpr int STSLOT = TX * TY;
+    static constexpr int OFF_C = K * USLOT;
+    static constexpr int OFF_ST = OFF_C + D * CSLOT;
+    static constexpr size_t BAR_OFF = size_t(OFF_ST + S * STSLOT) * 4;
+    static constexpr int NPUB = 32;  // B: per-plane completion; A: store-group completion
+    static constexpr int NBAR = 2 * (K + D + S) + NPUB;
+    static constexpr size_t SMEM = BAR_OFF + size_t(NBAR) * 8;
+    static_assert((TX * TY) % 128 == 0 && K >= 7 && D >= 1 && S >= 2, "shape");
+    static_assert(TX >= 8 && TY >= 5 && TX % 4 == 0 && RS <= 256 && ROWS <= 256, "TMA box / halo");
+};
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* tm, const void* src, int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+            reinterpret_cast<uint64_t>(tm)),
+        "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void add_sources_2s(const TB2SParams& p, uint64_t mask, int x, int z,
+                                               int n, float (&out)[4]) {
     while (mask) {
         const int s = __ffsll(static_cast<long long>(mask)) - 1;
         mask &= mask - 1;
@@ -94,283 +157,249 @@ __device__ __forceinline__ void add_sources_n(const TBParams& p, uint64_t mask, 
     }
 }
 
-template <int TX, int TY, int KA, int KB, int DA, int DB>
-struct TBShape {
-    static constexpr int NW = TX * TY / 128;  // consumer warps (4 points per thread)
-    static constexpr int NT = (NW + 3) * 32;  // + producer A, producer B, publisher
-    static constexpr int TXV = TX / 4;
-    static constexpr int RS = TX + 16;
-    static constexpr int ROWS = TY + 10;
-    static constexpr int USLOT = (RS * ROWS + 31) / 32 * 32;
-    static constexpr uint32_t UBYTES = RS * ROWS * 4;
-    static constexpr int CSLOT = 2 * TX * TY;  // u_prev tile then C tile
-    static constexpr uint32_t CBYTES = CSLOT * 4;
-    static constexpr int OFF_UB = KA * USLOT;
-    static constexpr int OFF_CA = OFF_UB + KB * USLOT;
-    static constexpr int OFF_CB = OFF_CA + DA * CSLOT;
-    static constexpr size_t BAR_OFF = size_t(OFF_CB + DB * CSLOT) * 4;
-    static constexpr int NPUB = 64;  // stage-A completion ring (> lag + 8: see the publisher)
-    static constexpr int NBAR = 2 * (KA + KB + DA + DB) + NPUB;
-    static constexpr size_t SMEM = BAR_OFF + size_t(NBAR) * 8;
-    static_assert((TX * TY) % 128 == 0, "whole consumer warps");
-    static_assert(KA >= 7 && KB >= 7, "6 live planes + 1 in flight");
-    static_assert(DA >= 1 && DB >= 1, "u_prev/C rings");
-    static_assert(TX >= 8 && TY >= 5, "halo reaches only the 4 edge-neighbour tiles");
-    static_assert(TX % 4 == 0 && RS <= 256 && ROWS <= 256 && TX <= 256 && TY <= 256, "TMA box");
-    static_assert(SMEM <= 232448, "shared memory");
-};
-
-template <int TX, int TY, int KA, int KB, int DA, int DB, int L, int U>
-__global__ void __launch_bounds__(TBShape<TX, TY, KA, KB, DA, DB>::NT, 1)
-    k_tb2(const __grid_constant__ CUtensorMap tmA_u, const __grid_constant__ CUtensorMap tmA_up,
-          const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tmB_u,
-          const __grid_constant__ CUtensorMap tmB_up, const __grid_constant__ TBParams p) {
-    using S = TBShape<TX, TY, KA, KB, DA, DB>;
-    static_assert(L >= 6 && L % U == 0, "lag: B plane j needs A planes <= j+5; B starts on a group");
-    static_assert(S::NPUB >= L + 16, "consumers run at most L + 6 planes ahead of the publisher");
+// W: TMA store groups whose writes may still be in flight when a plane is published (the
+// publication lag); staging slots (S_ = 4) are recycled as soon as a store has read them.
+// CH bit 0: stage A loads the u^n box and C with an evict_last L2 policy (stage B re-reads
+// u^n and C with evict_first: their last use).
+template <int TX, int TY, int K, int D, int U, int LMAX, int W, int CH>
+__global__ void __launch_bounds__(TB2SShape<TX, TY, K, D, 4>::NT, 2)
+    k_tb2s(const __grid_constant__ CUtensorMap tmA_u, const __grid_constant__ CUtensorMap tmA_up,
+           const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ CUtensorMap tmB_u,
+           const __grid_constant__ CUtensorMap tmB_up, const __grid_constant__ CUtensorMap tmA_st,
+           const __grid_constant__ TB2SParams p) {
+    constexpr int S_ = 4;
+    using S = TB2SShape<TX, TY, K, D, S_>;
+    static_assert(LMAX >= 7, "stage A may run at most LMAX planes ahead of stage B");
+    static_assert(W >= 1 && W < S::NPUB, "store groups in flight");
     extern __shared__ __align__(128) float smem[];
-    float* uA = smem;
-    float* uB = smem + S::OFF_UB;
-    float* cA = smem + S::OFF_CA;
-    float* cB = smem + S::OFF_CB;
+    float* uring = smem;
+    float* cring = smem + S::OFF_C;
+    float* stg = smem + S::OFF_ST;
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(smem) + S::BAR_OFF);
-    uint64_t* fullA = bars;
-    uint64_t* emptyA = fullA + KA;
-    uint64_t* fullB = emptyA + KA;
-    uint64_t* emptyB = fullB + KB;
-    uint64_t* fullCA = emptyB + KB;
-    uint64_t* emptyCA = fullCA + DA;
-    uint64_t* fullCB = emptyCA + DA;
-    uint64_t* emptyCB = fullCB + DB;
-    uint64_t* pubA = emptyCB + DB;  // pubA[i % NPUB]: all consumer warps finished A plane i
+    uint64_t* full_u = bars;
+    uint64_t* empty_u = full_u + K;
+    uint64_t* full_c = empty_u + K;
+    uint64_t* empty_c = full_c + D;
+    uint64_t* staged = empty_c + D;
+    uint64_t* stfree = staged + S_;
+    uint64_t* pub = stfree + S_;
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     if (tid == 0) {
-        for (int k = 0; k < KA; ++k) mbar_init(&fullA[k], 1), mbar_init(&emptyA[k], S::NW);
-        for (int k = 0; k < KB; ++k) mbar_init(&fullB[k], 1), mbar_init(&emptyB[k], S::NW);
-        for (int k = 0; k < DA; ++k) mbar_init(&fullCA[k], 1), mbar_init(&emptyCA[k], S::NW);
-        for (int k = 0; k < DB; ++k) mbar_init(&fullCB[k], 1), mbar_init(&emptyCB[k], S::NW);
-        for (int k = 0; k < S::NPUB; ++k) mbar_init(&pubA[k], S::NW);
+        for (int k = 0; k < K; ++k) mbar_init(&full_u[k], 1), mbar_init(&empty_u[k], S::NW);
+        for (int k = 0; k < D; ++k) mbar_init(&full_c[k], 1), mbar_init(&empty_c[k], S::NW);
+        for (int k = 0; k < S_; ++k) mbar_init(&staged[k], S::NW), mbar_init(&stfree[k], 1);
+        for (int k = 0; k < S::NPUB; ++k) mbar_init(&pub[k], (int)blockIdx.x < p.ntiles ? 1 : S::NW);
         fence_mbar_init();
     }
     __syncthreads();
 
+    const bool isA = (int)blockIdx.x < p.ntiles;
+    const int tile = isA ? blockIdx.x : blockIdx.x - p.ntiles;
     const int n = p.nzl;
-    const int tile = blockIdx.x;
     const int tyi = tile / p.tiles_x, txi = tile - tyi * p.tiles_x;
     const int x0 = txi * TX, y0 = p.ya_lo + tyi * TY;
     const unsigned long long E =
         (*reinterpret_cast<volatile const unsigned long long*>(p.d_epoch) * p.nbands + p.band + 1) << 32;
+    const CUtensorMap* tm_u = isA ? &tmA_u : &tmB_u;
+    const CUtensorMap* tm_up = isA ? &tmA_up : &tmB_up;
 
-    if (warp == S::NW) {  // ---------------- producer A: u^n boxes, (u^{n-1}, C) tiles
+    if (warp == S::NW) {  // ---------------- producer
         if (lane == 0) {
             const uint64_t pol_first = policy_evict_first();
-            auto put_u = [&](int j) {  // box plane j = buffer plane j (z = j - 5)
-                const uint32_t slot = j % KA;
-                if (j >= KA) mbar_wait_wd(smem_u32(&emptyA[slot]), ((j / KA) - 1) & 1);
-                mbar_expect_tx(&fullA[slot], S::UBYTES);
-                tma_load_3d(uA + slot * S::USLOT, &tmA_u, x0 - 8, y0 - 5, j, &fullA[slot]);
-            };
-            auto put_c = [&](int i) {  // u^{n-1} (read once) and C at plane i
-                const uint32_t slot = i % DA;
-                if (i >= DA) mbar_wait_wd(smem_u32(&emptyCA[slot]), ((i / DA) - 1) & 1);
-                mbar_expect_tx(&fullCA[slot], S::CBYTES);
-                float* dst = cA + slot * S::CSLOT;
-                tma_load_3d_hint(dst, &tmA_up, x0, y0, i + 5, &fullCA[slot], pol_first);
-                tma_load_3d(dst + TX * TY, &tm_c, x0, y0, i, &fullCA[slot]);
-            };
-            for (int j = 0; j < 10; ++j) put_u(j);
-            for (int i = 0; i < n; ++i) {
-                put_c(i);
-                put_u(i + 10);
-            }
-        }
-        return;
-    }
-    if (warp == S::NW + 1) {  // ---------------- producer B: u^{n+1} boxes, (u^n, C) tiles
-        if (lane == 0) {
-            const uint64_t pol_first = policy_evict_first();
-            // stage-A progress of this CTA and its edge neighbours (the box's x/y halo)
+            const uint64_t pol_last = policy_evict_last();
+            const bool keep = isA && (CH & 1);
             const unsigned long long* fl[5];
             int nfl = 0;
-            fl[nfl++] = p.flags + tile;
-            if (txi > 0) fl[nfl++] = p.flags + tile - 1;
-            if (txi + 1 < p.tiles_x) fl[nfl++] = p.flags + tile + 1;
-            if (tyi > 0) fl[nfl++] = p.flags + tile - p.tiles_x;
-            if (tyi + 1 < p.tiles_y) fl[nfl++] = p.flags + tile + p.tiles_x;
+            if (isA) {
+                fl[nfl++] = p.flagsB + tile;
+            } else {
+                fl[nfl++] = p.flagsA + tile;
+                if (txi > 0) fl[nfl++] = p.flagsA + tile - 1;
+                if (txi + 1 < p.tiles_x) fl[nfl++] = p.flagsA + tile + 1;
+                if (tyi > 0) fl[nfl++] = p.flagsA + tile - p.tiles_x;
+                if (tyi + 1 < p.tiles_y) fl[nfl++] = p.flagsA + tile + p.tiles_x;
+            }
             unsigned long long seen[5] = {0, 0, 0, 0, 0};
+            // A: throttle to B's progress (relaxed); B: acquire A's published planes
             auto wait_flags = [&](int need) {
+                if (need <= 0) return;
                 const unsigned long long want = E | (unsigned)need;
-                bool fenced = true;
+                bool fresh = false;
                 for (int k = 0; k < nfl; ++k) {
                     if (seen[k] >= want) continue;
-                    fenced = false;
-                    unsigned long long v = ld_acquire_gpu_u64(fl[k]);
+                    fresh = true;
+                    unsigned long long v = isA ? ld_relaxed_gpu_u64(fl[k]) : ld_acquire_gpu_u64(fl[k]);
                     if (v < want) {
                         const unsigned long long t0 = globaltimer_ns();
                         do {
                             __nanosleep(32);
-                            v = ld_acquire_gpu_u64(fl[k]);
+                            v = isA ? ld_relaxed_gpu_u64(fl[k]) : ld_acquire_gpu_u64(fl[k]);
                             if (v < want && globaltimer_ns() - t0 > kWatchdogNs) __trap();
                         } while (v < want);
                     }
                     seen[k] = v;
                 }
-                // generic-proxy stores (published) -> async-proxy (TMA) reads
-                if (!fenced) fence_proxy_async_global();
+                if (fresh && !isA) fence_proxy_async_global();
             };
             auto put_u = [&](int j) {
-                const uint32_t slot = j % KB;
-                if (j >= KB) mbar_wait_wd(smem_u32(&emptyB[slot]), ((j / KB) - 1) & 1);
-                mbar_expect_tx(&fullB[slot], S::UBYTES);
-                tma_load_3d(uB + slot * S::USLOT, &tmB_u, x0 - 8, y0 - 5, j, &fullB[slot]);
+                const uint32_t slot = j % K;
+                if (j >= K) mbar_wait_wd(smem_u32(&empty_u[slot]), ((j / K) - 1) & 1);
+                mbar_expect_tx(&full_u[slot], S::UBYTES);
+                if (keep)
+                    tma_load_3d_hint(uring + slot * S::USLOT, tm_u, x0 - 8, y0 - 5, j, &full_u[slot], pol_last);
+                else
+                    tma_load_3d(uring + slot * S::USLOT, tm_u, x0 - 8, y0 - 5, j, &full_u[slot]);
             };
-            auto put_c = [&](int i) {  // u^n and C at plane i: their last use
-                const uint32_t slot = i % DB;
-                if (i >= DB) mbar_wait_wd(smem_u32(&emptyCB[slot]), ((i / DB) - 1) & 1);
-                mbar_expect_tx(&fullCB[slot], S::CBYTES);
-                float* dst = cB + slot * S::CSLOT;
-                tma_load_3d_hint(dst, &tmB_up, x0, y0, i + 5, &fullCB[slot], pol_first);
-                tma_load_3d_hint(dst + TX * TY, &tm_c, x0, y0, i, &fullCB[slot], pol_first);
+            auto put_c = [&](int i) {  // u_prev (read once) and C at plane i
+                const uint32_t slot = i % D;
+                if (i >= D) mbar_wait_wd(smem_u32(&empty_c[slot]), ((i / D) - 1) & 1);
+                mbar_expect_tx(&full_c[slot], S::CBYTES);
+                float* dst = cring + slot * S::CSLOT;
+                tma_load_3d_hint(dst, tm_up, x0, y0, i + 5, &full_c[slot], pol_first);
+                if (keep)
+                    tma_load_3d_hint(dst + TX * TY, &tm_c, x0, y0, i, &full_c[slot], pol_last);
+                else if (isA)
+                    tma_load_3d(dst + TX * TY, &tm_c, x0, y0, i, &full_c[slot]);
+                else
+                    tma_load_3d_hint(dst + TX * TY, &tm_c, x0, y0, i, &full_c[slot], pol_first);
             };
-            wait_flags(n < 5 ? n : 5);
+            if (!isA) wait_flags(n < 5 ? n : 5);
             for (int j = 0; j < 10; ++j) put_u(j);
             for (int i = 0; i < n; ++i) {
-                wait_flags(i + 6 < n ? i + 6 : n);
+                if (isA) wait_flags(i - LMAX);
+                else wait_flags(i + 6 < n ? i + 6 : n);
                 put_c(i);
                 put_u(i + 10);
             }
         }
         return;
     }
-    if (warp == S::NW + 2) {  // ---------------- publisher: stage-A planes completed by the CTA
-        // Waits (acquire.cta) for plane i on pubA, folds in any later planes already complete,
-        // then releases flags[cta] at gpu scope: cumulative over the consumers' u^{n+1} stores.
-        // Safe ring reuse: a consumer reaches A plane i + NPUB only after B plane i + NPUB - L,
-        // which needs this CTA's flag >= i + NPUB - L + 6 > i + 1 (NPUB >= L + 16).
+    if (warp == S::NW + 1) {  // ---------------- A: TMA stores; B: progress (throttle)
         if (lane == 0) {
-            const uint32_t pb = smem_u32(pubA);
+            if (isA) {
+                // store plane i, recycle the slot of plane i - S_ + 1 once read, and signal
+                // pub[(i - W) % NPUB] once the writes of plane i - W are complete.  The gpu-scope
+                // release is left to the publisher warp: a release here would wait for every
+                // store this thread has in flight (MEMBAR.GPU), serialising the W-deep pipeline.
+                for (int i = 0; i < n; ++i) {
+                    const int slot = i % S_;
+                    mbar_wait_wd(smem_u32(&staged[slot]), (i / S_) & 1);
+                    tma_store_3d(&tmA_st, stg + slot * S::STSLOT, x0, y0, i + 5);
+                    bulk_commit();
+                    bulk_wait_read<S_ - 1>();  // the store of plane i - S_ + 1 has read its slot
+                    if (i >= S_ - 1) mbar_arrive(&stfree[(i - S_ + 1) % S_]);
+                    if (i >= W) {
+                        bulk_wait<W>();  // the writes of planes <= i - W are complete
+                        fence_proxy_async_global();
+                        mbar_arrive(&pub[(i - W) % S::NPUB]);
+                    }
+                }
+                bulk_wait<0>();
+                fence_proxy_async_global();
+                for (int i = n - W < 0 ? 0 : n - W; i < n; ++i) mbar_arrive(&pub[i % S::NPUB]);
+            } else {
+                int i = 0;
+                while (i < n) {
+                    mbar_wait_wd(smem_u32(&pub[i % S::NPUB]), (i / S::NPUB) & 1);
+                    ++i;
+                    while (i < n && mbar_try_wait(&pub[i % S::NPUB], (i / S::NPUB) & 1)) ++i;
+                    st_relaxed_gpu_u64(p.flagsB + tile, E | (unsigned)i);
+                }
+            }
+        }
+        return;
+    }
+    if (warp == S::NW + 2) {  // ---------------- A: publish completed u^{n+1} planes (acquire
+        if (lane == 0 && isA) {  // the store warp's completion, release at gpu scope)
             int i = 0;
             while (i < n) {
-                mbar_wait_wd(pb + 8 * (i % S::NPUB), (i / S::NPUB) & 1);
+                mbar_wait_wd(smem_u32(&pub[i % S::NPUB]), (i / S::NPUB) & 1);
                 ++i;
-                while (i < n && mbar_try_wait(&pubA[i % S::NPUB], (i / S::NPUB) & 1)) ++i;
-                st_release_gpu_u64(p.flags + tile, E | (unsigned)i);
+                while (i < n && mbar_try_wait(&pub[i % S::NPUB], (i / S::NPUB) & 1)) ++i;
+                fence_proxy_async_global();
+                st_release_gpu_u64(p.flagsA + tile, E | (unsigned)i);
             }
         }
         return;
     }
 
-    // ---------------- consumer warps: stage A on plane it, stage B on plane it - L
+    // ---------------- consumers (k_stream's loop, one stage)
     const int tx = tid % S::TXV, ty = tid / S::TXV;
     const int own = (5 + ty) * S::RS + 8 + 4 * tx;
     const int cown = ty * TX + 4 * tx;
     const float c[6] = {p.coef[0], p.coef[1], p.coef[2], p.coef[3], p.coef[4], p.coef[5]};
     const int x = x0 + 4 * tx, y = y0 + ty;
     const bool inx = x < p.nx;
-    const bool actA = inx && y < p.ya_hi && y < p.ny;
-    const bool actB = inx && y >= p.yb_lo && y < p.yb_hi;
-    const int nA = p.d_step[p.parity];  // samples of step n (A) and n+1 (B)
+    const bool actB = !isA && inx && y >= p.yb_lo && y < p.yb_hi;
+    const int nS = p.d_step[p.parity] + (isA ? 0 : 1);  // sample index of this stage's step
     uint64_t smask = 0;
-    if (actA) {
+    if (inx && y < p.ny) {  // A: every grid row it stores is exact (sources included)
         for (int s = 0; s < p.nsrc; ++s) {
             const DevSource& src = p.src[s];
             if (src.shot == 0 && src.y == y && src.x >= x && src.x < x + 4) smask |= (1ull << s);
         }
     }
     const long long col = (long long)y * p.nx + x;
-    float* outA = p.outA + 5 * p.plane + col;
     float* outB = p.outB + 5 * p.plane + col;
-    const uint32_t fA = smem_u32(fullA), eA = smem_u32(emptyA);
-    const uint32_t fB = smem_u32(fullB), eB = smem_u32(emptyB);
-    const uint32_t fCA = smem_u32(fullCA), eCA = smem_u32(emptyCA);
-    const uint32_t fCB = smem_u32(fullCB), eCB = smem_u32(emptyCB);
-    const uint32_t pub0 = smem_u32(pubA);
-    const float* uAown = uA + own;
-    const float* uBown = uB + own;
+    const uint32_t fu = smem_u32(full_u), eu = smem_u32(empty_u);
+    const uint32_t fc = smem_u32(full_c), ec = smem_u32(empty_c);
+    const uint32_t stg0 = smem_u32(staged), sfr0 = smem_u32(stfree), pub0 = smem_u32(pub);
+    const float* uown = uring + own;
 
-    float4 qA[10 + U], qB[10 + U];
+    float4 q[10 + U];
 #pragma unroll
     for (int j = 0; j < 10; ++j) {
-        mbar_wait_wd(fA + 8 * (j % KA), (j / KA) & 1);
-        qA[j] = *reinterpret_cast<const float4*>(uAown + (j % KA) * S::USLOT);
+        mbar_wait_wd(fu + 8 * (j % K), (j / K) & 1);
+        q[j] = *reinterpret_cast<const float4*>(uown + (j % K) * S::USLOT);
         if (j < 5) {
             __syncwarp();
-            if (lane == 0) mbar_arrive_u32(eA + 8 * (j % KA));
+            if (lane == 0) mbar_arrive_u32(eu + 8 * (j % K));
         }
     }
-    uint32_t snA = 10 % KA, pnA = (10 / KA) & 1, scA = 5 % KA, sqA = 0, pqA = 0;
-    uint32_t snB = 10 % KB, pnB = (10 / KB) & 1, scB = 5 % KB, sqB = 0, pqB = 0;
-    const int total = n + L;
+    uint32_t sn = 10 % K, pn = (10 / K) & 1, sc = 5 % K, sq = 0, pq = 0;
     int it = 0;
     auto body = [&](auto OFF) {
         constexpr int O = decltype(OFF)::value;
-        if (it < n) {  // ---- stage A: u^{n+1} at plane it
-            mbar_wait_wd(fA + 8 * snA, pnA);
-            qA[O + 10] = *reinterpret_cast<const float4*>(uAown + snA * S::USLOT);
-            mbar_wait_wd(fCA + 8 * sqA, pqA);
-            const float* cb = cA + sqA * S::CSLOT + cown;
-            const float4 upv = *reinterpret_cast<const float4*>(cb);
-            const float4 cv = *reinterpret_cast<const float4*>(cb + TX * TY);
-            float out[4];
-            star4<S::RS, O>(uAown + scA * S::USLOT, qA, upv, cv, c, out);
+        mbar_wait_wd(fu + 8 * sn, pn);
+        q[O + 10] = *reinterpret_cast<const float4*>(uown + sn * S::USLOT);
+        mbar_wait_wd(fc + 8 * sq, pq);
+        const float* cb = cring + sq * S::CSLOT + cown;
+        const float4 upv = *reinterpret_cast<const float4*>(cb);
+        const float4 cv = *reinterpret_cast<const float4*>(cb + TX * TY);
+        float out[4];
+        star4<S::RS, O>(uown + sc * S::USLOT, q, upv, cv, c, out);
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive_u32(eu + 8 * sc);
+            mbar_arrive_u32(ec + 8 * sq);
+        }
+        if (smask) add_sources_2s(p, smask, x, it, nS, out);
+        const float4 o4 = make_float4(out[0], out[1], out[2], out[3]);
+        if (isA) {
+            const int slot = it % S_;
+            if (it >= S_) mbar_wait_wd(sfr0 + 8 * slot, ((it / S_) - 1) & 1);
+            *reinterpret_cast<float4*>(stg + slot * S::STSLOT + cown) = o4;
+            fence_proxy_async_smem();  // generic smem writes -> the TMA store's async reads
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive_u32(eA + 8 * scA);
-                mbar_arrive_u32(eCA + 8 * sqA);
-            }
-            if (smask) add_sources_n(p, smask, x, it, nA, out);
-            if (actA) __stcg(reinterpret_cast<float4*>(outA), make_float4(out[0], out[1], out[2], out[3]));
-            __syncwarp();  // the lanes' stores, then one release.cta arrive for the warp
+            if (lane == 0) mbar_arrive_u32(stg0 + 8 * slot);
+        } else {
+            if (actB) st_stream4(outB, o4);
+            __syncwarp();
             if (lane == 0) mbar_arrive_u32(pub0 + 8 * (it % S::NPUB));
-            if (++snA == KA) snA = 0, pnA ^= 1;
-            if (++scA == KA) scA = 0;
-            if (++sqA == DA) sqA = 0, pqA ^= 1;
-            outA += p.plane;
         }
-        if (it >= L) {  // ---- stage B: u^{n+2} at plane it - L
-            mbar_wait_wd(fB + 8 * snB, pnB);
-            qB[O + 10] = *reinterpret_cast<const float4*>(uBown + snB * S::USLOT);
-            mbar_wait_wd(fCB + 8 * sqB, pqB);
-            const float* cb = cB + sqB * S::CSLOT + cown;
-            const float4 upv = *reinterpret_cast<const float4*>(cb);
-            const float4 cv = *reinterpret_cast<const float4*>(cb + TX * TY);
-            float out[4];
-            star4<S::RS, O>(uBown + scB * S::USLOT, qB, upv, cv, c, out);
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive_u32(eB + 8 * scB);
-                mbar_arrive_u32(eCB + 8 * sqB);
-            }
-            if (smask) add_sources_n(p, smask, x, it - L, nA + 1, out);
-            if (actB) st_stream4(outB, make_float4(out[0], out[1], out[2], out[3]));
-            if (++snB == KB) snB = 0, pnB ^= 1;
-            if (++scB == KB) scB = 0;
-            if (++sqB == DB) sqB = 0, pqB ^= 1;
-            outB += p.plane;
-        }
+        if (++sn == K) sn = 0, pn ^= 1;
+        if (++sc == K) sc = 0;
+        if (++sq == D) sq = 0, pq ^= 1;
+        outB += p.plane;
         ++it;
     };
 #pragma unroll 1
-    for (int i = 0; i < total; i += U) {
-        if (i == L) {  // stage-B queue prologue: u^{n+1} planes z = -5 .. 4
+    for (int i = 0; i < n; i += U) {
+        if (!unrolled<0, U>(body, i, n)) break;
 #pragma unroll
-            for (int j = 0; j < 10; ++j) {
-                mbar_wait_wd(fB + 8 * (j % KB), (j / KB) & 1);
-                qB[j] = *reinterpret_cast<const float4*>(uBown + (j % KB) * S::USLOT);
-                if (j < 5) {
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_u32(eB + 8 * (j % KB));
-                }
-            }
-        }
-        if (!unrolled<0, U>(body, i, total)) break;
-#pragma unroll
-        for (int o = 0; o < 10; ++o) {
-            qA[o] = qA[o + U];
-            qB[o] = qB[o + U];
-        }
+        for (int o = 0; o < 10; ++o) q[o] = q[o + U];
     }
 }
 
@@ -380,44 +409,45 @@ __global__ void k_tb_advance(int* d_step, int parity, unsigned long long* d_epoc
 }
 
 // ------------------------------------------------------------------------------------
-template <int TX, int TY, int KA, int KB, int DA, int DB, int L, int U>
-static cudaError_t tb_prepare(const void** fn, int* threads, size_t* smem) {
-    using S = TBShape<TX, TY, KA, KB, DA, DB>;
-    *fn = reinterpret_cast<const void*>(&k_tb2<TX, TY, KA, KB, DA, DB, L, U>);
+template <int TX, int TY, int K, int D, int U, int LMAX, int W, int CH>
+static cudaError_t tb2s_prepare(const void** fn, int* threads, size_t* smem) {
+    using S = TB2SShape<TX, TY, K, D, 4>;
+    *fn = reinterpret_cast<const void*>(&k_tb2s<TX, TY, K, D, U, LMAX, W, CH>);
     *threads = S::NT;
     *smem = S::SMEM;
     return cudaFuncSetAttribute(*fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(*smem));
 }
 
-cudaError_t tb_variant_fn(int id, const void** fn, int* threads, size_t* smem) {
+cudaError_t tb2s_variant_fn(int id, const void** fn, int* threads, size_t* smem) {
     switch (id) {
-#define X(vid, name, tx, ty, ka, kb, da, db, l, u, pair) \
-    case vid:                                            \
-        return tb_prepare<tx, ty, ka, kb, da, db, l, u>(fn, threads, smem);
-        RTM_TB_VARIANTS(X)
+#define X(vid, name, tx, ty, k, d, u, lmax, w, ch, pair) \
+    case vid:                                              \
+        return tb2s_prepare<tx, ty, k, d, u, lmax, w, ch>(fn, threads, smem);
+        RTM_TB2S_VARIANTS(X)
 #undef X
         default:
             return cudaErrorInvalidValue;
     }
 }
 
-cudaError_t launch_tb2(int id, const CUtensorMap tm[5], const TBParams& p, cudaStream_t s) {
+cudaError_t launch_tb2s(int id, const CUtensorMap tm[6], const TB2SParams& p, cudaStream_t s) {
     const void* fn;
     int threads;
     size_t smem;
-    cudaError_t e = tb_variant_fn(id, &fn, &threads, &smem);
+    cudaError_t e = tb2s_variant_fn(id, &fn, &threads, &smem);
     if (e != cudaSuccess) return e;
     void* args[] = {const_cast<CUtensorMap*>(&tm[0]), const_cast<CUtensorMap*>(&tm[1]),
                     const_cast<CUtensorMap*>(&tm[2]), const_cast<CUtensorMap*>(&tm[3]),
-                    const_cast<CUtensorMap*>(&tm[4]), const_cast<TBParams*>(&p)};
+                    const_cast<CUtensorMap*>(&tm[4]), const_cast<CUtensorMap*>(&tm[5]),
+                    const_cast<TB2SParams*>(&p)};
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(p.tiles_x * p.tiles_y));
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * p.ntiles));
     cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident, or a launch error
+    attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
