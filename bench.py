@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--nsteps", type=int, default=0, help="override the config's time steps")
     ap.add_argument("--shots", type=int, default=1,
                     help="batched independent shots on the config's velocity model (f3)")
+    ap.add_argument("--halo", type=int, default=0, choices=[0, 2],
+                    help="N > 1 halo exchange: 0 NCCL send/recv (default), 2 fused push over "
+                         "CUDA-IPC peer stores + flag protocol (SURVEY §8(f) f1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="short run for ncu captures (no extras)")
@@ -233,6 +236,8 @@ def main():
         tdist.broadcast_object_list(uid, src=0)
         h = P.rtm_create_dist(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32, rank, world,
                               uid[0], local)
+        if args.halo:
+            P.rtm_set_option(h, P.RTM_OPT_HALO_MODE, args.halo)  # collective
     elif args.shots > 1:
         z0, nzl = 0, cfg.nz
         h = P.rtm_create_batch(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32, args.shots)
@@ -378,6 +383,8 @@ def main():
             "config": {"workload": wl, "grid": [cfg.nx, cfg.ny, cfg.nz], "time_steps": nsteps,
                        "sources": len(cfg.sources_xyz), "shots": shots,
                        "parallelism": f"z-slab x{world}",
+                       "halo": ("fused IPC push + flags" if args.halo == 2 else "NCCL send/recv")
+                       if world > 1 else None,
                        "tile": tile_name, "l2": "inputs larger than L2 (3 x 4 GiB fields)"
                        if pts_local * 4 > 126e6 else "L2-resident (no flush)"},
             "hbm_effective_gbs": round(value * bytes_per_pt, 1),

@@ -138,10 +138,20 @@ const char* rtm_tile_name(int tile_id);  /* e.g. "stream64x32k10d0"; NULL for un
  *   RTM_OPT_SHOT_ORDER batched contexts: 0 auto (shot-major when C fits in 40% of L2), 1 shot-major
  *                      (each shot's tiles co-run), 2 shot-fastest (co-running CTAs share C tiles)
  *   RTM_OPT_CHECK_EVERY 0 (default) off; k > 0: rtm_step checks the field for NaN/Inf every k steps
- *   RTM_OPT_HALO_MODE  in-process multi-slab contexts: 0 (default) boundary planes first + halo copies
- *                      on copy engines overlapped with the interior; 1 fused push — one kernel per
- *                      slab whose epilogue stores the boundary planes straight into the neighbours'
- *                      halos (peer stores over NVLink; needs peer access, else RTM_EINVAL)
+ *   RTM_OPT_HALO_MODE  slab contexts:
+ *                      0 (default) boundary planes first, halo copies (in-process: copy engines;
+ *                        distributed: NCCL send/recv on a comm stream) overlapped with the interior;
+ *                      1 in-process only: fused push — one kernel per slab whose epilogue stores
+ *                        the boundary planes straight into the neighbours' halos (peer stores over
+ *                        NVLink), ordered by CUDA events;
+ *                      2 fused push ordered by a flag protocol: after each step a 1-thread kernel
+ *                        releases "steps done" (system scope) into the neighbours' flag words and
+ *                        the next step's stream waits on its own flags (cuStreamWaitValue64; no
+ *                        spinning kernel).  In a distributed context the neighbours' buffers and
+ *                        flags are CUDA-IPC mappings (same node, peer access) set up by an NCCL
+ *                        all-gather of the handles: setting it there is a COLLECTIVE call, as is
+ *                        rtm_set_step_count while it is active.  Needs 64-bit stream memory ops.
+ *                      Peer access is required between neighbouring devices (else RTM_EINVAL).
  *   RTM_OPT_TB_CTAS    two-step variants ("tb2_*"): max CTAs per y-band launch,
  *                      0 (default) = one per SM.  Smaller values force more, narrower bands
  *                      (used by the tests to cover band edges on small grids).

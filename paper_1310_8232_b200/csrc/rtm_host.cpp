@@ -106,6 +106,15 @@ struct Slab {
     unsigned long long* d_epoch = nullptr;     // pass epoch (never reset)
     cudaGraphExec_t tb_graph[4] = {nullptr, nullptr, nullptr, nullptr};  // key bank*2 + parity
     int tb_graph_variant[4] = {-1, -1, -1, -1};
+    // fused halo push with the flag protocol (halo mode 2): the neighbours' time-level buffers
+    // and flag words — direct pointers in-process, CUDA-IPC mappings across processes
+    unsigned long long* d_sig = nullptr;       // [2]: steps completed by the lo / hi neighbour
+    float* nb_lo[2] = {nullptr, nullptr};
+    float* nb_hi[2] = {nullptr, nullptr};
+    int nb_lo_nzl = 0;
+    unsigned long long* nb_lo_sig = nullptr;   // the lo neighbour's d_sig (we write its [1])
+    unsigned long long* nb_hi_sig = nullptr;   // the hi neighbour's d_sig (we write its [0])
+    std::vector<void*> ipc_open;               // mappings to cudaIpcCloseMemHandle
     cudaStream_t stream() const { return has_user ? s_user : s_own; }
 };
 
@@ -126,7 +135,11 @@ struct rtm_ctx {
     int zchunk = 0;  // 0 = auto
     int cache_mode = 0x41;  // L2 prefetch of u_prev/C 4 planes ahead, evict_last (tuned)
     int shot_order = 0;     // 0 auto, 1 shot-major, 2 shot-fastest
-    int halo_mode = 0;      // multi-slab: 0 copy engines (cudaMemcpyPeerAsync), 1 fused push
+    int halo_mode = 0;      // slabs: 0 boundary first + copies / NCCL, 1 fused push (events,
+                            // in-process), 2 fused push + flag protocol (in-process or IPC)
+    unsigned long long sig_gen = 0;  // flag generation (bumped at every synchronising reset)
+    bool sig_fresh = true;           // first step of a generation: no flag waits
+    unsigned sig_flush = 0;          // CU_STREAM_WAIT_VALUE_FLUSH when the devices support it
     int check_every = 0;    // NaN/Inf scan every k steps (0 = off)
     int tb_ctas = 0;        // two-step passes: max CTAs per band (0 = #SMs)
     int l2_bytes = 0;
@@ -156,6 +169,18 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
             fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
     }
     return fn;
+}
+
+typedef CUresult (*PFN_waitv64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*PFN_devattr)(int*, CUdevice_attribute, CUdevice);
+template <class F>
+F driver_fn(const char* name) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+        return reinterpret_cast<F>(p);
+    return nullptr;
 }
 
 bool finite_coeffs(const float c[6]) {
@@ -240,6 +265,8 @@ void free_slab(Slab& s) {
     }
     if (s.d_flags) cudaFree(s.d_flags);
     if (s.d_epoch) cudaFree(s.d_epoch);
+    for (void* q : s.ipc_open) cudaIpcCloseMemHandle(q);
+    if (s.d_sig) cudaFree(s.d_sig);
     if (s.C) cudaFree(s.C);
     if (s.d_step) cudaFree(s.d_step);
     if (s.d_stats) cudaFree(s.d_stats);
@@ -796,9 +823,150 @@ int step_slabs_fused(rtm_ctx* c, int nsteps) {
     return RTM_OK;
 }
 
+// Halo mode 2 set-up: flag words per slab, neighbours' buffer / flag pointers.  In-process
+// (mode 1) they are the other slabs' allocations; across processes (mode 2, one rank per GPU)
+// every rank exports CUDA-IPC handles of its two time-level buffers and its flag words, the
+// handles are all-gathered over the context's NCCL communicator (a collective call) and the
+// neighbours' are opened (cudaIpcMemLazyEnablePeerAccess: NVLink peer mappings).
+struct IpcRecord {
+    cudaIpcMemHandle_t buf[2];
+    cudaIpcMemHandle_t sig;
+    int nzl;
+    int pad[15];
+};
+static_assert(sizeof(IpcRecord) == 256, "IPC record size");
+
+int setup_signal(rtm_ctx* c) {
+    static PFN_devattr devattr = driver_fn<PFN_devattr>("cuDeviceGetAttribute");
+    if (!devattr) return fail(RTM_ECUDA, "cuDeviceGetAttribute unavailable from the driver");
+    unsigned flush = CU_STREAM_WAIT_VALUE_FLUSH;
+    for (auto& s : c->slabs) {
+        int mem64 = 0, fl = 0;
+        devattr(&mem64, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, (CUdevice)s.dev);
+        devattr(&fl, CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES, (CUdevice)s.dev);
+        if (!mem64) return fail(RTM_EINVAL, "device %d has no 64-bit stream memory operations", s.dev);
+        if (!fl) flush = 0;
+        CK(cudaSetDevice(s.dev));
+        if (!s.d_sig) CK(cudaMalloc(&s.d_sig, 2 * sizeof(unsigned long long)));
+        CK(cudaMemset(s.d_sig, 0, 2 * sizeof(unsigned long long)));
+    }
+    c->sig_flush = flush;
+    const int G = (int)c->slabs.size();
+    if (c->mode == 1) {
+        for (int r = 0; r < G; ++r) {
+            Slab& s = c->slabs[r];
+            if (s.lo_nb) {
+                const Slab& n = c->slabs[r - 1];
+                s.nb_lo[0] = n.buf[0], s.nb_lo[1] = n.buf[1], s.nb_lo_nzl = n.nzl, s.nb_lo_sig = n.d_sig;
+            }
+            if (s.hi_nb) {
+                const Slab& n = c->slabs[r + 1];
+                s.nb_hi[0] = n.buf[0], s.nb_hi[1] = n.buf[1], s.nb_hi_sig = n.d_sig;
+            }
+        }
+    } else if (c->mode == 2) {
+        Slab& s = c->slabs[0];
+        CK(cudaSetDevice(s.dev));
+        IpcRecord mine;
+        std::memset(&mine, 0, sizeof mine);
+        for (int b = 0; b < 2; ++b) CK(cudaIpcGetMemHandle(&mine.buf[b], s.buf[b]));
+        CK(cudaIpcGetMemHandle(&mine.sig, s.d_sig));
+        mine.nzl = s.nzl;
+        const int W = c->world;
+        unsigned char* d = nullptr;
+        CK(cudaMalloc(&d, (size_t)W * sizeof(IpcRecord)));
+        std::vector<IpcRecord> all(W);
+        int rc = RTM_OK;
+        if (cudaMemcpy(d + (size_t)c->rank * sizeof(IpcRecord), &mine, sizeof mine,
+                       cudaMemcpyHostToDevice) != cudaSuccess)
+            rc = fail(RTM_ECUDA, "IPC record upload failed");
+        if (rc == RTM_OK) {
+            const ncclResult_t nr = ncclAllGather(d + (size_t)c->rank * sizeof(IpcRecord), d,
+                                                  sizeof(IpcRecord), ncclUint8, c->comm, s.stream());
+            if (nr != ncclSuccess) rc = fail(RTM_ENCCL, "ncclAllGather of IPC handles: %s", ncclGetErrorString(nr));
+        }
+        if (rc == RTM_OK && (cudaStreamSynchronize(s.stream()) != cudaSuccess ||
+                             cudaMemcpy(all.data(), d, (size_t)W * sizeof(IpcRecord),
+                                        cudaMemcpyDeviceToHost) != cudaSuccess))
+            rc = fail(RTM_ECUDA, "IPC record gather failed");
+        cudaFree(d);
+        RET(rc);
+        auto open = [&](const cudaIpcMemHandle_t& hd, void** out) -> int {
+            const cudaError_t e = cudaIpcOpenMemHandle(out, hd, cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) return fail(RTM_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+            s.ipc_open.push_back(*out);
+            return RTM_OK;
+        };
+        if (s.ipc_open.empty()) {
+            void* q;
+            if (s.lo_nb) {
+                const IpcRecord& n = all[c->rank - 1];
+                for (int b = 0; b < 2; ++b) {
+                    RET(open(n.buf[b], &q));
+                    s.nb_lo[b] = static_cast<float*>(q);
+                }
+                RET(open(n.sig, &q));
+                s.nb_lo_sig = static_cast<unsigned long long*>(q);
+                s.nb_lo_nzl = n.nzl;
+            }
+            if (s.hi_nb) {
+                const IpcRecord& n = all[c->rank + 1];
+                for (int b = 0; b < 2; ++b) {
+                    RET(open(n.buf[b], &q));
+                    s.nb_hi[b] = static_cast<float*>(q);
+                }
+                RET(open(n.sig, &q));
+                s.nb_hi_sig = static_cast<unsigned long long*>(q);
+            }
+        }
+    }
+    ++c->sig_gen;
+    c->sig_fresh = true;
+    return RTM_OK;
+}
+
+// G > 1 step, fused halo push + flag protocol (f1, halo mode 2; across processes in mode 2):
+// step n on slab r waits (stream-side cuStreamWaitValue64, no spinning kernel) until both
+// neighbours have completed step n-1 — their pushes into r's halo have landed (RAW) and their
+// step n-1 reads of the halo planes r now overwrites are done (WAR) — then one stencil launch
+// whose epilogue also stores r's boundary planes into the neighbours' halos (peer / IPC
+// stores over NVLink), then k_signal releases "steps done = n+1" into the neighbours' flags.
+// Values carry a generation (bumped by every synchronising reset), so stale flags never pass.
+int step_slabs_signal(rtm_ctx* c, int nsteps) {
+    static PFN_waitv64 waitv = driver_fn<PFN_waitv64>("cuStreamWaitValue64");
+    if (!waitv) return fail(RTM_ECUDA, "cuStreamWaitValue64 unavailable from the driver");
+    const size_t plane = (size_t)c->nx * c->ny;
+    const unsigned long long g = c->sig_gen << 40;
+    for (int k = 0; k < nsteps; ++k) {
+        const int parity = (int)(c->step & 1);
+        const unsigned long long n = (unsigned long long)c->step;
+        for (auto& s : c->slabs) {
+            CK(cudaSetDevice(s.dev));
+            cudaStream_t st = s.stream();
+            if (!c->sig_fresh) {
+                for (int side = 0; side < 2; ++side)
+                    if (side == 0 ? s.lo_nb : s.hi_nb) {
+                        const CUresult r = waitv((CUstream)st, (CUdeviceptr)(s.d_sig + side), g | n,
+                                                 CU_STREAM_WAIT_VALUE_GEQ | c->sig_flush);
+                        if (r != CUDA_SUCCESS) return fail(RTM_ECUDA, "cuStreamWaitValue64 failed (%d)", (int)r);
+                    }
+            }
+            float* lo = s.lo_nb ? s.nb_lo[parity ^ 1] + (size_t)(s.nb_lo_nzl + 5) * plane : nullptr;
+            float* hi = s.hi_nb ? s.nb_hi[parity ^ 1] : nullptr;
+            RET(launch_stencil(c, s, parity, 0, s.nzl, 0, 0, 1, st, lo, hi));
+            CK(launch_signal(s.lo_nb ? s.nb_lo_sig + 1 : nullptr, s.hi_nb ? s.nb_hi_sig : nullptr,
+                             g | (n + 1), st));
+        }
+        c->sig_fresh = false;
+        ++c->step;
+    }
+    return RTM_OK;
+}
+
 // G > 1 step: boundary planes first, exchange on the comm stream, interior concurrently.
 int step_slabs(rtm_ctx* c, int nsteps) {
     if (c->mode == 1 && c->halo_mode == 1) return step_slabs_fused(c, nsteps);
+    if (c->halo_mode == 2) return step_slabs_signal(c, nsteps);
     const int G = (int)c->slabs.size();
     for (int k = 0; k < nsteps; ++k) {
         const int parity = (int)(c->step & 1);
@@ -914,6 +1082,8 @@ int reset_impl(rtm_ctx* c, const float* u, const float* up) {
         CK(cudaMemsetAsync(s.d_step, 0, 2 * sizeof(int), st));
     }
     c->step = 0;
+    ++c->sig_gen;  // synchronising (halo exchange + sync below): flags restart
+    c->sig_fresh = true;
     // G > 1: fill the halo planes of u^0 and u^{-1} from the neighbours' initial data
     if (c->slabs.size() > 1 || c->mode == 2) {
         for (int par = 0; par < 2; ++par) {
@@ -1309,6 +1479,8 @@ int rtm_set_step_count(rtm_ctx* c, long long n) {
     if ((n & 1) != (c->step & 1))
         for (auto& s : c->slabs) {
             std::swap(s.buf[0], s.buf[1]);
+            std::swap(s.nb_lo[0], s.nb_lo[1]);  // every slab / rank swaps alike
+            std::swap(s.nb_hi[0], s.nb_hi[1]);
             s.tm_variant = -1;  // tensor maps follow the buffers
             s.graph_valid = false;
             for (int k = 0; k < 4; ++k) s.tb_graph_variant[k] = -1;
@@ -1319,6 +1491,20 @@ int rtm_set_step_count(rtm_ctx* c, long long n) {
         CK(cudaMemcpy(s.d_step, h, sizeof h, cudaMemcpyHostToDevice));
     }
     c->step = n;
+    if (c->halo_mode == 2) {  // flags restart: make the call collective across ranks
+        if (c->comm) {
+            Slab& s = c->slabs[0];
+            CK(cudaSetDevice(s.dev));
+            double* d = nullptr;
+            CK(cudaMalloc(&d, sizeof(double)));
+            const ncclResult_t nr = ncclAllReduce(d, d, 1, ncclFloat64, ncclSum, c->comm, s.stream());
+            const cudaError_t e = cudaStreamSynchronize(s.stream());
+            cudaFree(d);
+            if (nr != ncclSuccess || e != cudaSuccess) return fail(RTM_ENCCL, "set_step_count barrier failed");
+        }
+        ++c->sig_gen;
+        c->sig_fresh = true;
+    }
     return RTM_OK;
 }
 
@@ -1393,10 +1579,12 @@ int rtm_set_option(rtm_ctx* c, int key, long long value) {
             c->tb_ctas = (int)value;
             break;
         case RTM_OPT_HALO_MODE:
-            if (value < 0 || value > 1) return fail(RTM_EINVAL, "halo mode %lld not in 0..1", value);
+            if (value < 0 || value > 2) return fail(RTM_EINVAL, "halo mode %lld not in 0..2", value);
             if (value == 1 && c->mode != 1)
-                return fail(RTM_EINVAL, "the fused halo push needs an in-process multi-slab context");
-            if (value == 1) {  // every slab must be able to store into its neighbours' memory
+                return fail(RTM_EINVAL, "halo mode 1 (fused push, event ordered) needs an in-process multi-slab context");
+            if (value == 2 && c->mode == 0)
+                return fail(RTM_EINVAL, "halo mode 2 (fused push, flag protocol) needs a multi-slab or distributed context");
+            if (value >= 1 && c->mode == 1) {  // every slab must be able to store into its neighbours
                 for (size_t r = 0; r + 1 < c->slabs.size(); ++r) {
                     const int a = c->slabs[r].dev, b = c->slabs[r + 1].dev;
                     int ab = 1, ba = 1;
@@ -1408,9 +1596,10 @@ int rtm_set_option(rtm_ctx* c, int key, long long value) {
                         return fail(RTM_EINVAL, "devices %d and %d have no peer access", a, b);
                 }
             }
-            {  // switch cleanly: drain, and refill the halos of both levels from the owners
+            {  // switch cleanly: drain first (mode 2 contexts: a collective call)
                 DeviceGuard g;
                 RET(sync_all(c));
+                if (value == 2) RET(setup_signal(c));
                 c->halo_mode = (int)value;
             }
             break;

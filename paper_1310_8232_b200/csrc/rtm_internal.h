@@ -118,5 +118,8 @@ cudaError_t launch_field_stats(const float* buf, long long plane, int nzl, int n
                                unsigned int* stats, cudaStream_t s);
 cudaError_t launch_velocity(const float* v, float* C, long long n, double dt, double dx,
                             unsigned int* stats, cudaStream_t s);
+// st.release.sys of v into *lo and *hi (either may be null) after a system fence
+cudaError_t launch_signal(unsigned long long* lo, unsigned long long* hi, unsigned long long v,
+                          cudaStream_t s);
 
 }  // namespace rtm

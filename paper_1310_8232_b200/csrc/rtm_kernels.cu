@@ -762,6 +762,23 @@ cudaError_t launch_field_stats(const float* buf, long long plane, int nzl, int n
     return cudaGetLastError();
 }
 
+// Fused-push step signal (f1, flag protocol): after a slab's stencil launch has completed (stream
+// order), publish "steps done" to the neighbours' flag words (peer / CUDA-IPC device memory) with
+// a system-scope fence + release store, so their next step's stream wait (cuStreamWaitValue64)
+// sees the halo planes this step pushed into them.
+__global__ void k_signal(unsigned long long* lo, unsigned long long* hi, unsigned long long v) {
+    __threadfence_system();
+    if (lo) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(lo), "l"(v) : "memory");
+    if (hi) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(hi), "l"(v) : "memory");
+}
+
+cudaError_t launch_signal(unsigned long long* lo, unsigned long long* hi, unsigned long long v,
+                          cudaStream_t s) {
+    if (!lo && !hi) return cudaSuccess;
+    k_signal<<<1, 1, 0, s>>>(lo, hi, v);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_velocity(const float* v, float* C, long long n, double dt, double dx,
                             unsigned int* stats, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;

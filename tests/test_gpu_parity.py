@@ -175,10 +175,13 @@ def test_graph_and_direct_launch_paths_agree(P):
 
 
 # ----------------------------------------------------------------------------- slabs
-@pytest.mark.parametrize("G,halo", [(2, 0), (3, 0), (4, 0), (2, 1), (3, 1), (4, 1)])
+@pytest.mark.parametrize("G,halo", [(2, 0), (3, 0), (4, 0), (2, 1), (3, 1), (4, 1), (2, 2), (3, 2),
+                                    (4, 2)])
 def test_multislab_on_one_gpu_bitwise_equals_single(P, G, halo):
-    """z-slab decomposition (boundary planes first, halo copies, interior) on one GPU gives
-    exactly the G=1 field (R14)."""
+    """z-slab decomposition on one GPU gives exactly the G=1 field (R14): halo mode 0
+    (boundary planes first, halo copies, interior), 1 (fused push, event ordered), 2 (fused
+    push, flag protocol: stream waits on flag words + system-scope release kernels — the
+    protocol the distributed context uses across processes)."""
     nz, ny, nx = 47, 33, 72
     rng = np.random.default_rng(G)
     v = rng.uniform(1500, 4300, (nz, ny, nx)).astype(np.float32)
@@ -202,16 +205,46 @@ def test_multislab_on_one_gpu_bitwise_equals_single(P, G, halo):
     assert relerr(got, orc) <= TOL_1 * 10
 
 
-def test_dist_world1_equals_single(P):
+@pytest.mark.parametrize("halo", [0, 2])
+def test_dist_world1_equals_single(P, halo):
+    """The NCCL-communicator context at world 1; halo mode 2 runs its collective set-up (IPC
+    handle export + NCCL all-gather) and the flag-protocol step path."""
     nz, ny, nx = 20, 16, 32
     v = np.full((nz, ny, nx), 2000.0, np.float32)
     u0, up0 = ri.random_fields(v.shape, seed=3)
     ref = gpu_run(P, v, 10.0, 1e-3, 6, u0=u0, up0=up0)
     uid = P.rtm_get_unique_id()
     with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, dist=(0, 1, uid, 0)) as sim:
+        P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, halo)
         sim.set_velocity(v)
         sim.set_fields(u0, up0)
         sim.step(6)
+        assert np.array_equal(sim.read_field(), ref)
+        P.rtm_set_step_count(sim.h, 3)  # collective barrier + flag generation restart
+        sim.set_fields(u0, up0)
+        sim.step(2)
+
+
+@pytest.mark.parametrize("halo", [1, 2])
+def test_multislab_fused_resume_and_reset(P, halo):
+    """Flag generations: reset / set_fields / rtm_set_step_count restart the protocol (stale
+    flags never satisfy a wait), including a parity swap of the time levels."""
+    cfg = ri.make_config(2, shape=(40, 24, 64), steps=20)
+    v = cfg.velocity()
+    src = cfg.sources()
+    ref = gpu_run(P, v, cfg.dx, cfg.dt, 20, sources=src)
+    with P.Simulation(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, C32, devices=[0, 0, 0]) as sim:
+        P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, halo)
+        sim.set_velocity(v)
+        for s in src:
+            sim.inject_source(*s)
+        sim.step(9)
+        u, up = sim.read_fields()
+        sim.reset()
+        sim.step(3)
+        sim.set_fields(u, up)
+        P.rtm_set_step_count(sim.h, 9)
+        sim.step(11)
         assert np.array_equal(sim.read_field(), ref)
 
 
@@ -467,8 +500,10 @@ def test_batch_errors(P):
 
 def test_fused_halo_mode_rejected_without_slabs(P):
     with P.Simulation(16, 16, 16, 10.0, 1e-3, C32) as sim:
-        with pytest.raises(P.RtmError):
-            P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, 1)
+        for mode in (1, 2, 3, -1):
+            with pytest.raises(P.RtmError):
+                P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, mode)
+        assert P.rtm_get_option(sim.h, P.RTM_OPT_HALO_MODE) == 0
 
 
 # ----------------------------------------------------------------------------- full-size properties
