@@ -110,6 +110,28 @@ int rtm_field_stats(rtm_ctx* ctx, double* max_abs, long long* nonfinite);
 int rtm_set_velocity_device(rtm_ctx* ctx, const float* d_v);
 int rtm_read_field_device(rtm_ctx* ctx, float* d_out);
 
+/* Asynchronous host-buffer pipeline (single-slab contexts: single-GPU, batched, or one rank of
+ * a distributed context).  These calls only ENQUEUE work and return; host buffers must stay
+ * valid and unmodified (v) / unread (out) until the next rtm_sync.  Pinned host memory makes
+ * the copies truly asynchronous: the H2D of the next velocity and the D2H of the previous result
+ * then overlap the stencil steps (an H2D and a D2H copy stream plus a device staging buffer and
+ * a device snapshot buffer, each nx*ny*nz floats, allocated on first use).
+ *   rtm_set_velocity_async: H2D of v into the staging buffer, then a1 (C(p) and the validity /
+ *       CFL reduction) on the context's stream after the work already enqueued; steps enqueued
+ *       afterwards use the new model.  The verdict (RTM_EINVAL non-finite/non-positive values,
+ *       RTM_ECFL) is DEFERRED to the next rtm_sync (or synchronising call: rtm_step,
+ *       rtm_set_velocity), which then returns it and marks the velocity unset; steps run in
+ *       between used the rejected model.
+ *   rtm_step_async: rtm_step without the final synchronisation (no field check / profiling).
+ *   rtm_read_field_async: snapshot of u^n (device copy, ordered after the steps enqueued so
+ *       far) and its D2H into out on the copy stream.
+ *   rtm_sync: waits for everything enqueued (the context's stream is made to wait for the copy
+ *       streams) and returns the first deferred error. */
+int rtm_set_velocity_async(rtm_ctx* ctx, const float* v);
+int rtm_step_async(rtm_ctx* ctx, int nsteps);
+int rtm_read_field_async(rtm_ctx* ctx, float* out);
+int rtm_sync(rtm_ctx* ctx);
+
 /* Kernel variant ("tile", the GPU analogue of the paper's blocksize):
  * -1 = automatic (default), 0 = naive one-thread-per-point kernel, 1..rtm_num_tiles()-1 =
  * TMA-staged xy tiles.  Unknown id -> RTM_EINVAL.  Every variant computes bitwise-identical

@@ -154,6 +154,13 @@ struct rtm_ctx {
     float last_ms = 0;
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     int num_sms = 148;
+    // asynchronous host-buffer pipeline (single-slab contexts; rtm_*_async, rtm_sync)
+    cudaStream_t s_copy = nullptr;  // D2H of results
+    cudaStream_t s_h2d = nullptr;   // H2D of velocities (separate: it must not queue behind a D2H)
+    cudaEvent_t ev_h2d = nullptr, ev_conv = nullptr, ev_snap = nullptr, ev_d2h = nullptr;
+    float* v_stage = nullptr;   // H2D staging of the next velocity (nx*ny*nz floats)
+    float* snap = nullptr;      // device snapshot of u^n for the D2H (nshots*nx*ny*nz floats)
+    bool vcheck_pending = false;  // deferred CFL / validity verdict of async velocities
 };
 
 namespace {
@@ -294,6 +301,15 @@ void destroy_ctx(rtm_ctx* c) {
     for (auto e : c->prof_ev) cudaEventDestroy(e);
     if (c->t0) cudaEventDestroy(c->t0);
     if (c->t1) cudaEventDestroy(c->t1);
+    for (cudaStream_t q : {c->s_copy, c->s_h2d})
+        if (q) {
+            cudaStreamSynchronize(q);
+            cudaStreamDestroy(q);
+        }
+    for (cudaEvent_t e : {c->ev_h2d, c->ev_conv, c->ev_snap, c->ev_d2h})
+        if (e) cudaEventDestroy(e);
+    if (c->v_stage) cudaFree(c->v_stage);
+    if (c->snap) cudaFree(c->snap);
     for (auto& s : c->slabs) free_slab(s);
     delete c;
 }
@@ -1024,7 +1040,10 @@ int h2d_planes(rtm_ctx* c, Slab& s, float* dst_base, const float* host, cudaStre
     return RTM_OK;
 }
 
+int async_vcheck(rtm_ctx* c);
+
 int set_velocity_impl(rtm_ctx* c, const float* v, bool device_ptr) {
+    RET(async_vcheck(c));  // verdict of earlier rtm_set_velocity_async calls (synchronising)
     c->vel_set = false;
     const size_t plane = (size_t)c->nx * c->ny;
     for (auto& s : c->slabs) {
@@ -1110,6 +1129,52 @@ int read_impl(rtm_ctx* c, float* out, int which /*0 = u^n, 1 = u^{n-1}*/) {
                                plane * s.nzl * sizeof(float), cudaMemcpyDeviceToHost, s.stream()));
     }
     return sync_all(c);
+}
+
+// The asynchronous pipeline's copy stream, events and staging buffers (lazily, single slab).
+int async_setup(rtm_ctx* c, bool need_stage, bool need_snap) {
+    if (c->slabs.size() != 1) return fail(RTM_EINVAL, "the asynchronous calls need a single-slab context");
+    Slab& s = c->slabs[0];
+    CK(cudaSetDevice(s.dev));
+    if (!c->s_copy) {
+        CK(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+        for (cudaEvent_t* e : {&c->ev_h2d, &c->ev_conv, &c->ev_snap, &c->ev_d2h})
+            CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    const size_t n = (size_t)c->nx * c->ny * s.nzl;
+    if (need_stage && !c->v_stage && cudaMalloc(&c->v_stage, n * sizeof(float)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(RTM_ENOMEM, "velocity staging buffer (%zu bytes)", n * 4);
+    }
+    if (need_snap && !c->snap && cudaMalloc(&c->snap, n * s.nshots * sizeof(float)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(RTM_ENOMEM, "readback snapshot buffer (%zu bytes)", n * s.nshots * 4);
+    }
+    return RTM_OK;
+}
+
+// Deferred verdict of the velocities given to rtm_set_velocity_async since the last check
+// (d_stats accumulates max v and the invalid count over all of them).  Host-synchronising.
+int async_vcheck(rtm_ctx* c) {
+    if (!c->vcheck_pending) return RTM_OK;
+    c->vcheck_pending = false;
+    Slab& s = c->slabs[0];
+    unsigned int hs[2];
+    CK(cudaMemcpyAsync(hs, s.d_stats, sizeof hs, cudaMemcpyDeviceToHost, s.stream()));
+    CK(cudaStreamSynchronize(s.stream()));
+    float m;
+    std::memcpy(&m, &hs[0], 4);
+    if (hs[1]) {
+        c->vel_set = false;
+        return fail(RTM_EINVAL, "an asynchronous velocity had %u non-finite or non-positive values", hs[1]);
+    }
+    const double nu = (double)m * (double)c->dt / (double)c->dx;
+    if (nu > c->nu_crit) {
+        c->vel_set = false;
+        return fail(RTM_ECFL, "an asynchronous velocity violated CFL: max(v)*dt/dx = %.6f > %.6f", nu, c->nu_crit);
+    }
+    return RTM_OK;
 }
 
 }  // namespace
@@ -1415,7 +1480,7 @@ int rtm_step(rtm_ctx* c, int nsteps) {
     CK(cudaEventElapsedTime(&c->last_ms, c->t0, c->t1));
     RET(collect_profile(c));
     c->prof_launches = 0;
-    return RTM_OK;
+    return async_vcheck(c);
 }
 
 int rtm_read_field(rtm_ctx* c, float* out) {
@@ -1813,5 +1878,75 @@ int rtm_kernel_stats(rtm_ctx* c, long long* launches, double* total_ms) {
 }
 
 long long rtm_launch_count(rtm_ctx* c) { return c ? c->launches : -1; }
+
+int rtm_set_velocity_async(rtm_ctx* c, const float* v) {
+    if (!c || !v) return fail(RTM_EINVAL, "NULL argument");
+    DeviceGuard g;
+    RET(async_setup(c, true, false));
+    Slab& s = c->slabs[0];
+    const size_t n = (size_t)c->nx * c->ny * s.nzl;
+    cudaStream_t st = s.stream();
+    if (!c->vcheck_pending) CK(cudaMemsetAsync(s.d_stats, 0, 2 * sizeof(unsigned int), st));
+    CK(cudaStreamWaitEvent(c->s_h2d, c->ev_conv, 0));  // the previous conversion read v_stage
+    CK(cudaMemcpyAsync(c->v_stage, v, n * sizeof(float), cudaMemcpyHostToDevice, c->s_h2d));
+    CK(cudaEventRecord(c->ev_h2d, c->s_h2d));
+    CK(cudaStreamWaitEvent(st, c->ev_h2d, 0));  // C changes after the steps already enqueued
+    CK(launch_velocity(c->v_stage, s.C, (long long)n, (double)c->dt, (double)c->dx, s.d_stats, st));
+    CK(cudaEventRecord(c->ev_conv, st));
+    c->vcheck_pending = true;
+    c->vel_set = true;  // provisional: rtm_sync returns the verdict
+    return RTM_OK;
+}
+
+int rtm_step_async(rtm_ctx* c, int nsteps) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    if (nsteps < 0) return fail(RTM_EINVAL, "nsteps must be >= 0");
+    if (!c->vel_set) return fail(RTM_ESTATE, "rtm_step_async before a velocity was set");
+    if (c->slabs.size() != 1) return fail(RTM_EINVAL, "the asynchronous calls need a single-slab context");
+    if (c->check_every > 0 || c->profiling)
+        return fail(RTM_ESTATE, "rtm_step_async with the field check or profiling on (use rtm_step)");
+    DeviceGuard g;
+    CK(cudaSetDevice(c->slabs[0].dev));
+    c->prof_launches = 0;
+    if (c->mode == 0) return step_single(c, nsteps);
+    return step_slabs(c, nsteps);
+}
+
+int rtm_read_field_async(rtm_ctx* c, float* out) {
+    if (!c || !out) return fail(RTM_EINVAL, "NULL argument");
+    DeviceGuard g;
+    RET(async_setup(c, false, true));
+    Slab& s = c->slabs[0];
+    const size_t plane = (size_t)c->nx * c->ny, n = plane * s.nzl;
+    cudaStream_t st = s.stream();
+    CK(cudaStreamWaitEvent(st, c->ev_d2h, 0));  // the previous D2H has read the snapshot
+    for (int k = 0; k < s.nshots; ++k)
+        CK(cudaMemcpyAsync(c->snap + (size_t)k * n, s.buf[c->step & 1] + ((size_t)k * (s.nzl + 10) + 5) * plane,
+                           n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    CK(cudaEventRecord(c->ev_snap, st));
+    CK(cudaStreamWaitEvent(c->s_copy, c->ev_snap, 0));
+    CK(cudaMemcpyAsync(out, c->snap, n * s.nshots * sizeof(float), cudaMemcpyDeviceToHost, c->s_copy));
+    CK(cudaEventRecord(c->ev_d2h, c->s_copy));
+    return RTM_OK;
+}
+
+int rtm_sync(rtm_ctx* c) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    DeviceGuard g;
+    Slab& s = c->slabs[0];
+    CK(cudaSetDevice(s.dev));
+    if (c->s_copy) {  // the context's stream ends after the last asynchronous copies
+        CK(cudaEventRecord(c->ev_d2h, c->s_copy));
+        CK(cudaStreamWaitEvent(s.stream(), c->ev_d2h, 0));
+        CK(cudaEventRecord(c->ev_h2d, c->s_h2d));
+        CK(cudaStreamWaitEvent(s.stream(), c->ev_h2d, 0));
+    }
+    RET(sync_all(c));
+    if (c->s_copy) {
+        CK(cudaStreamSynchronize(c->s_copy));
+        CK(cudaStreamSynchronize(c->s_h2d));
+    }
+    return async_vcheck(c);
+}
 
 }  // extern "C"

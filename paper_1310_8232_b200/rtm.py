@@ -82,6 +82,10 @@ _SIGS = {
     "rtm_nu_crit": (_D, [_P]),
     "rtm_autotune": (_I, [_P, _I, _P, _P, _I, ctypes.POINTER(rtm_tune_result), _P]),
     "rtm_select_mwmb": (_I, [_P, _I, _I]),
+    "rtm_set_velocity_async": (_I, [_P, _P]),
+    "rtm_step_async": (_I, [_P, _I]),
+    "rtm_read_field_async": (_I, [_P, _P]),
+    "rtm_sync": (_I, [_P]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)
@@ -183,6 +187,33 @@ def rtm_field_stats(h):
     m, bad = _D(0), _LL(0)
     _check(lib.rtm_field_stats(h, ctypes.byref(m), ctypes.byref(bad)))
     return float(m.value), int(bad.value)
+
+
+def _async_buf(a, name, write=False):
+    # no implicit conversion copy: the library reads/writes the caller's memory after return
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags.c_contiguous
+            and (a.flags.writeable or not write)):
+        raise ValueError(f"{name} must be a C-contiguous float32 array"
+                         + (" (writeable)" if write else ""))
+    return _ptr(a)
+
+
+def rtm_set_velocity_async(h, v):
+    """v must stay alive and unmodified until rtm_sync (keep a reference)."""
+    return _check(lib.rtm_set_velocity_async(h, _async_buf(v, "v")))
+
+
+def rtm_step_async(h, nsteps):
+    return _check(lib.rtm_step_async(h, int(nsteps)))
+
+
+def rtm_read_field_async(h, out):
+    """out: a C-contiguous float32 array, filled once rtm_sync returns."""
+    return _check(lib.rtm_read_field_async(h, _async_buf(out, "out", write=True)))
+
+
+def rtm_sync(h):
+    return _check(lib.rtm_sync(h))
 
 
 def rtm_set_velocity_device(h, dptr: int):

@@ -720,3 +720,60 @@ def test_full_size_c4_tb2_sampled(P):
                     rng.integers(0, nz, 50_000)], 1).astype(np.int32)
     ref1 = oracle.points_f32(v, cfg.dx, cfg.dt, C32, u0, up0, pts)
     assert relerr(u1[pts[:, 2], pts[:, 1], pts[:, 0]], ref1) <= TOL_1
+
+
+# ----------------------------------------------------------------------------- asynchronous pipeline
+def test_async_pipeline_equals_sync_calls(P):
+    """rtm_set_velocity_async / rtm_step_async / rtm_read_field_async pipelined over several
+    velocity models (H2D of the next model and D2H of the previous result overlap the steps)
+    give bitwise the results of the synchronous calls; mixing in a synchronous call works."""
+    nz, ny, nx = 30, 40, 64
+    rng = np.random.default_rng(12)
+    models = [rng.uniform(1500, 4300, (nz, ny, nx)).astype(np.float32) for _ in range(3)]
+    w = ri.source_samples(3000.0, 1e-3, 15.0, 20)
+    src = [(30, 20, 15, w)]
+    refs = [gpu_run(P, v, 10.0, 1e-3, 17, sources=src) for v in models]
+    outs = [np.empty((nz, ny, nx), np.float32) for _ in models]
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32) as sim:
+        for s in src:
+            sim.inject_source(*s)
+        for v, o in zip(models, outs):
+            P.rtm_set_velocity_async(sim.h, v)
+            P.rtm_reset(sim.h)
+            P.rtm_step_async(sim.h, 17)
+            P.rtm_read_field_async(sim.h, o)
+        P.rtm_sync(sim.h)
+        for o, r in zip(outs, refs):
+            assert np.array_equal(o, r)
+        sim.set_velocity(models[1])           # synchronous call after asynchronous ones
+        sim.reset()
+        P.rtm_step_async(sim.h, 17)
+        assert np.array_equal(sim.read_field(), refs[1])
+        with pytest.raises(ValueError):
+            P.rtm_read_field_async(sim.h, np.empty((nz, ny, nx), np.float64))
+
+
+def test_async_velocity_verdict_is_deferred(P):
+    nz, ny, nx = 12, 16, 32
+    good = np.full((nz, ny, nx), 2000.0, np.float32)
+    bad = np.full((nz, ny, nx), 4600.0, np.float32)  # nu = 0.46 > nu_crit = 0.4419 at dt = 1 ms
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32) as sim:
+        P.rtm_set_velocity_async(sim.h, good)
+        P.rtm_step_async(sim.h, 2)
+        P.rtm_sync(sim.h)
+        P.rtm_set_velocity_async(sim.h, bad)
+        P.rtm_step_async(sim.h, 2)
+        with pytest.raises(P.RtmError) as e:
+            P.rtm_sync(sim.h)
+        assert e.value.code == P.RTM_ECFL
+        with pytest.raises(P.RtmError) as e:
+            P.rtm_step_async(sim.h, 1)       # the velocity is unset after the verdict
+        assert e.value.code == P.RTM_ESTATE
+        nan = good.copy()
+        nan[3, 4, 5] = np.nan
+        P.rtm_set_velocity_async(sim.h, nan)
+        with pytest.raises(P.RtmError) as e:
+            sim.set_velocity(good)             # a synchronising call returns the pending verdict
+        assert e.value.code == P.RTM_EINVAL
+        sim.set_velocity(good)
+        sim.step(1)
