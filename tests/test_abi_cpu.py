@@ -136,3 +136,19 @@ def test_select_mwmb_is_eq2_minmax(P):
     m = np.array([[np.nan, 5.0, 4.0], [1.0, 4.0, 6.0]])
     assert P.rtm_select_mwmb(m) == 1  # a candidate that failed anywhere is never chosen
     assert P.rtm_select_mwmb(np.array([[2.0, 2.0]])) == 0  # ties -> lowest index
+
+
+def test_async_calls_validate_before_device(P):
+    """The asynchronous calls read/write caller memory after returning, so the binding refuses
+    arrays it would have to convert (a temporary copy would die first); NULL contexts are
+    rejected by the library itself (no device needed)."""
+    with pytest.raises(ValueError):
+        P.rtm_read_field_async(None, np.empty(8, np.float64))
+    with pytest.raises(ValueError):
+        P.rtm_set_velocity_async(None, np.ones((2, 4), np.float32)[:, ::2])
+    for fn, args in ((P.rtm_sync, ()), (P.rtm_step_async, (1,)),
+                     (P.rtm_read_field_async, (np.empty(4, np.float32),)),
+                     (P.rtm_set_velocity_async, (np.ones(4, np.float32),))):
+        with pytest.raises(P.RtmError) as e:
+            fn(None, *args)
+        assert e.value.code == P.RTM_EINVAL

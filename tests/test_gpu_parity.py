@@ -777,3 +777,35 @@ def test_async_velocity_verdict_is_deferred(P):
         assert e.value.code == P.RTM_EINVAL
         sim.set_velocity(good)
         sim.step(1)
+
+
+def test_async_pipeline_batched_shots_and_dist_world1(P):
+    """The asynchronous calls on a batched (2-shot) context and on a distributed context at
+    world 1: same bits as the synchronous path."""
+    nz, ny, nx = 20, 24, 32
+    rng = np.random.default_rng(21)
+    v = rng.uniform(1500, 4300, (nz, ny, nx)).astype(np.float32)
+    w = ri.source_samples(3000.0, 1e-3, 15.0, 12)
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, shots=2) as sim:
+        P.rtm_inject_source_shot(sim.h, 0, 5, 6, 7, w)
+        P.rtm_inject_source_shot(sim.h, 1, 20, 12, 9, -w)
+        sim.set_velocity(v)
+        sim.step(11)
+        ref = sim.read_field()
+        out = np.empty_like(ref)
+        P.rtm_set_velocity_async(sim.h, v)
+        P.rtm_reset(sim.h)
+        P.rtm_step_async(sim.h, 11)
+        P.rtm_read_field_async(sim.h, out)
+        P.rtm_sync(sim.h)
+        assert np.array_equal(out, ref)
+    ref1 = gpu_run(P, v, 10.0, 1e-3, 11, sources=[(5, 6, 7, w)])
+    uid = P.rtm_get_unique_id()
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, dist=(0, 1, uid, 0)) as sim:
+        sim.inject_source(5, 6, 7, w)
+        out = np.empty((nz, ny, nx), np.float32)
+        P.rtm_set_velocity_async(sim.h, v)
+        P.rtm_step_async(sim.h, 11)
+        P.rtm_read_field_async(sim.h, out)
+        P.rtm_sync(sim.h)
+        assert np.array_equal(out, ref1)
