@@ -100,6 +100,23 @@ def test_c3_full_grid_20_steps_vs_oracle(P):
     assert relerr(got, ref) <= TOL_FULL
 
 
+@pytest.mark.parametrize("k", [3, 5, 4])
+def test_full_size_full_step_count_vs_oracle(P, k):
+    """BASELINE.json north_star: "<= 1e-4 max|u| after the config's full step count" — the
+    config's own recipe (zero ICs, its velocity model and Ricker sources) at full size and full
+    step count: C3 512^3 x 200, C5 (G=1) 1024x1024x256 x 100, C4 1024^3 x 100 (16 shots'
+    sources), every point against the fp32 oracle on all host cores (C4: ~2-3 min of CPU)."""
+    cfg = ri.make_config(k)
+    v = cfg.velocity()
+    src = cfg.sources()
+    got = gpu_run(P, v, cfg.dx, cfg.dt, cfg.steps, sources=src)
+    ref = oracle.run(v, cfg.dx, cfg.dt, C32, cfg.steps, sources=src)
+    assert np.abs(ref).max() > 0
+    e = relerr(got, ref)
+    print(f"C{k} {v.shape} {cfg.steps} steps: max|d|/max|u| = {e:.3e}")
+    assert e <= TOL_FULL
+
+
 @pytest.mark.parametrize("k", [4, 5])
 def test_full_size_one_step_sampled(P, k):
     """Full BASELINE sizes (C4 1024^3, C5 1024x1024x256), in the bench's launch config:

@@ -1,6 +1,7 @@
 """Small cases for compute-sanitizer (memcheck / racecheck / synccheck): every kernel family
-(naive, k_tiled, k_stream with and without the u_prev/C ring, batched shots, slabs with copy
-and fused halo modes) on ragged grids of 16^3-64^3."""
+(naive, k_tiled, k_stream with and without the u_prev/C ring, the two-step k_tb2s, batched
+shots, slabs with copy, fused and flag-protocol halo modes, the asynchronous pipeline) on
+ragged grids of 16^3-64^3."""
 import sys
 from pathlib import Path
 
@@ -11,7 +12,7 @@ import paper_1310_8232_b200 as P  # noqa: E402
 import rtm_inputs as ri  # noqa: E402
 
 
-def run(shape, tile, steps=3, shots=1, devices=None, halo=0):
+def run(shape, tile, steps=3, shots=1, devices=None, halo=0, tb_ctas=0):
     nz, ny, nx = shape
     v = np.full(shape, 2500.0, np.float32)
     u0, up0 = ri.random_fields(shape, seed=1)
@@ -21,6 +22,8 @@ def run(shape, tile, steps=3, shots=1, devices=None, halo=0):
             P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, halo)
         if tile is not None:
             sim.set_tile(tile)
+        if tb_ctas:
+            P.rtm_set_option(sim.h, P.RTM_OPT_TB_CTAS, tb_ctas)
         sim.set_velocity(v)
         sim.inject_source(nx // 2, ny // 2, nz // 2, w)
         if shots > 1:
@@ -42,4 +45,18 @@ if __name__ == "__main__":
     run((19, 30, 64), names["stream64x16k8d4u11"], shots=3)
     run((40, 24, 32), None, devices=[0, 0])
     run((40, 24, 32), None, devices=[0, 0, 0], halo=1)
+    run((40, 24, 32), None, devices=[0, 0, 0], halo=2)
+    tb = [i for n, i in names.items() if n.startswith("tb2s_")][0]
+    run((21, 37, 68), tb, steps=5)
+    run((13, 61, 130), tb, steps=4, tb_ctas=6)       # several y-bands
+    shape = (12, 20, 40)
+    v = np.full(shape, 2500.0, np.float32)
+    out = np.empty(shape, np.float32)
+    with P.Simulation(40, 20, 12, 10.0, 1e-3, ri.COEFFS_F32) as sim:   # asynchronous pipeline
+        for _ in range(2):
+            P.rtm_set_velocity_async(sim.h, v)
+            P.rtm_reset(sim.h)
+            P.rtm_step_async(sim.h, 3)
+            P.rtm_read_field_async(sim.h, out)
+        P.rtm_sync(sim.h)
     print("sanitize cases done")
