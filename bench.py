@@ -430,6 +430,11 @@ def main():
                          "alg_bytes_per_launch": int(alg_bytes // max(kl, 1)),
                          "traffic_source": traffic_src},
             "e2e": e2e, "gpu_launches": gpu_launches, "clocks": clocks.summary(),
+            "paper_context": {"note": "context only (other hardware, CPU, no GPU numbers in the paper)",
+                              "source": "PAPER.md:559-560 Table ExecTime3, 200x200x800 x 448 it.",
+                              "hardware": "2x Xeon E5410 quad-core 2.33 GHz (PAPER.md:478)",
+                              "efficient_blocksize_1core_gpts": 0.0612,
+                              "efficient_blocksize_8core_gpts": 0.235},
             "autotune": tune,
             "cpu_baseline": cpu, "finite": finite,
         }

@@ -48,7 +48,7 @@ if __name__ == "__main__":
     run((40, 24, 32), None, devices=[0, 0, 0], halo=2)
     tb = [i for n, i in names.items() if n.startswith("tb2s_")][0]
     run((21, 37, 68), tb, steps=5)
-    run((13, 61, 130), tb, steps=4, tb_ctas=6)       # several y-bands
+    run((13, 61, 132), tb, steps=4, tb_ctas=6)       # several y-bands
     shape = (12, 20, 40)
     v = np.full(shape, 2500.0, np.float32)
     out = np.empty(shape, np.float32)
