@@ -266,7 +266,7 @@ def main():
         # stream-kernel variant timed on this grid (max over ranks = MWMB), winner verified
         P.rtm_set_velocity_device(h, d_v.data_ptr())
         cands = [t for t in range(P.rtm_num_tiles())
-                 if (P.rtm_tile_name(t) or "").startswith(("stream", "tb2"))]
+                 if (P.rtm_tile_name(t) or "").startswith(("stream", "tb2", "resident"))]
         res, times = P.rtm_autotune(h, args.tune_ni, tiles=cands)
         tune = {"selected": P.rtm_tile_name(res["best_tile"]), "candidates": len(cands),
                 "nI": args.tune_ni, "min_time_ms": round(res["min_time_ms"], 4),
@@ -416,7 +416,7 @@ def main():
                          "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4) if achieved else None,
                          "traffic": traffic, "peak_source": peak_src,
-                         "kernel": ("k_tb2s" if two_step else
+                         "kernel": ("k_tb2s" if two_step else "k_resident" if tile_name.startswith("resident") else
                                     "k_stream" if tile_name.startswith(("stream", "tb2")) else
                                     "k_tiled" if tile_name.startswith("tma") else "k_naive")
                                    + f"<{tile_name}>", "launches": kl,

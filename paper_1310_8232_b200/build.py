@@ -18,7 +18,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "librtm_b200.so"
-SOURCES = [CSRC / "rtm_kernels.cu", CSRC / "rtm_tb.cu", CSRC / "rtm_host.cpp"]
+SOURCES = [CSRC / "rtm_kernels.cu", CSRC / "rtm_tb.cu", CSRC / "rtm_resident.cu", CSRC / "rtm_host.cpp"]
 HEADERS = [CSRC / "rtm_internal.h", CSRC / "rtm_device.cuh", ROOT / "include" / "rtm.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -66,7 +66,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
                 raise RuntimeError(f"nvcc failed: {' '.join(r.args)}")
     tmp = LIB.with_suffix(f".so.tmp{os.getpid()}")
     link = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-L", str(lib),
-            "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}", "-lcuda" if False else "-lcudart_static"]
+            "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}", "-lcudart_static"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode:
         sys.stderr.write(r.stdout + r.stderr)

@@ -196,30 +196,15 @@ __device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* t
         : "memory");
 }
 
-// The k_stream per-thread update of 4 x-consecutive points at the centre plane: `row` points at
-// the thread's own 4 points in the staged (RS-float rows, 5-row y halo, 8-float x halo) plane,
-// q[O + k] = u at z offset k - 5 (register queue), upv/cv = u_prev and C.  Same operations in
-// the same order as k_stream's loop body, so the two kernels are bitwise identical.
-template <int RS, int O, int N>
-__device__ __forceinline__ void star4(const float* row, const float4 (&q)[N], float4 upv, float4 cv,
-                                      const float (&c)[6], float (&out)[4]) {
-    float xs[14];
-    {
-        const float4 l = *reinterpret_cast<const float4*>(row - 4);
-        const float4 rr = *reinterpret_cast<const float4*>(row + 4);
-        xs[0] = row[-5];
-        xs[1] = l.x; xs[2] = l.y; xs[3] = l.z; xs[4] = l.w;
-        xs[5] = q[O + 5].x; xs[6] = q[O + 5].y; xs[7] = q[O + 5].z; xs[8] = q[O + 5].w;
-        xs[9] = rr.x; xs[10] = rr.y; xs[11] = rr.z; xs[12] = rr.w;
-        xs[13] = row[8];
-    }
-    float4 yv[11];
-#pragma unroll
-    for (int m = 1; m <= 5; ++m) {
-        yv[5 - m] = *reinterpret_cast<const float4*>(row - m * RS);
-        yv[5 + m] = *reinterpret_cast<const float4*>(row + m * RS);
-    }
-    yv[5] = q[O + 5];
+// The k_stream per-thread update of 4 x-consecutive points, split into the operand gather
+// (from shared memory in k_stream / k_tb2s, from L2 in k_resident) and ONE arithmetic core, so
+// every kernel performs the same operations in the same order (bitwise-identical results).
+// q[O + k] = u at z offset k - 5 (register queue); yv[5 +- m] = u at y offset +-m (yv[5] =
+// q[O + 5]); xs[0..13] = u at x offsets -5 .. +8 of the first point; upv/cv = u_prev and C.
+template <int O, int N>
+__device__ __forceinline__ void star4_core(const float4 (&q)[N], const float4 (&yv)[11],
+                                           const float (&xs)[14], float4 upv, float4 cv,
+                                           const float (&c)[6], float (&out)[4]) {
     const float4 L4 = make_float4(xs[1], xs[2], xs[3], xs[4]);
     const float4 R4 = make_float4(xs[9], xs[10], xs[11], xs[12]);
     float2 xa[5], xb[5];
@@ -244,6 +229,31 @@ __device__ __forceinline__ void star4(const float* row, const float4 (&q)[N], fl
     const float2 ra = rtm_point2(za, ya, xa, lo2(upv), lo2(cv), c);
     const float2 rb = rtm_point2(zb, yb, xb, hi2(upv), hi2(cv), c);
     out[0] = ra.x; out[1] = ra.y; out[2] = rb.x; out[3] = rb.y;
+}
+
+// Operands from a staged plane: `row` points at the thread's own 4 points in the (RS-float
+// rows, 5-row y halo, 8-float x halo) shared-memory copy of the centre plane.
+template <int RS, int O, int N>
+__device__ __forceinline__ void star4(const float* row, const float4 (&q)[N], float4 upv, float4 cv,
+                                      const float (&c)[6], float (&out)[4]) {
+    float xs[14];
+    {
+        const float4 l = *reinterpret_cast<const float4*>(row - 4);
+        const float4 rr = *reinterpret_cast<const float4*>(row + 4);
+        xs[0] = row[-5];
+        xs[1] = l.x; xs[2] = l.y; xs[3] = l.z; xs[4] = l.w;
+        xs[5] = q[O + 5].x; xs[6] = q[O + 5].y; xs[7] = q[O + 5].z; xs[8] = q[O + 5].w;
+        xs[9] = rr.x; xs[10] = rr.y; xs[11] = rr.z; xs[12] = rr.w;
+        xs[13] = row[8];
+    }
+    float4 yv[11];
+#pragma unroll
+    for (int m = 1; m <= 5; ++m) {
+        yv[5 - m] = *reinterpret_cast<const float4*>(row - m * RS);
+        yv[5 + m] = *reinterpret_cast<const float4*>(row + m * RS);
+    }
+    yv[5] = q[O + 5];
+    star4_core<O>(q, yv, xs, upv, cv, c, out);
 }
 
 }  // namespace rtm

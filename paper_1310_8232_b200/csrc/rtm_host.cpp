@@ -104,6 +104,7 @@ struct Slab {
     int bank = 0;                              // toggled at every bank swap
     unsigned long long* d_flags = nullptr;     // stage-A progress per CTA of a band
     unsigned long long* d_epoch = nullptr;     // pass epoch (never reset)
+    unsigned* d_bar = nullptr;                 // k_resident grid barrier [2]
     cudaGraphExec_t tb_graph[4] = {nullptr, nullptr, nullptr, nullptr};  // key bank*2 + parity
     int tb_graph_variant[4] = {-1, -1, -1, -1};
     // fused halo push with the flag protocol (halo mode 2): the neighbours' time-level buffers
@@ -271,6 +272,7 @@ void free_slab(Slab& s) {
         if (s.alt[b]) cudaFree(s.alt[b]);
     }
     if (s.d_flags) cudaFree(s.d_flags);
+    if (s.d_bar) cudaFree(s.d_bar);
     if (s.d_epoch) cudaFree(s.d_epoch);
     for (void* q : s.ipc_open) cudaIpcCloseMemHandle(q);
     if (s.d_sig) cudaFree(s.d_sig);
@@ -588,7 +590,7 @@ bool tb_plan(const rtm_ctx* c, const TileVariant& tv, int* tiles_x, std::vector<
 
 bool tb_active(const rtm_ctx* c) {
     const int v = resolve_tile(c);
-    if (variant(v).kind < 3) return false;
+    if (variant(v).kind != 4) return false;
     int tx;
     std::vector<TBBand> b;
     return tb_plan(c, variant(v), &tx, &b);
@@ -718,12 +720,53 @@ int upload_sources(rtm_ctx* c, Slab& s) {
     return RTM_OK;
 }
 
+// Resident multi-step launches (kind 5): the whole run in cooperative launches of up to 4096
+// steps, one grid barrier per step inside.
+int step_resident(rtm_ctx* c, int nsteps) {
+    Slab& s = c->slabs[0];
+    cudaStream_t st = s.stream();
+    const TileVariant& tv = variant(resolve_tile(c));
+    int occ = variant_occupancy(resolve_tile(c), nullptr);
+    if (occ < 1) return fail(RTM_ECUDA, "variant %s cannot be resident", tv.name);
+    const int ctas = c->num_sms * std::min(occ, tv.MINB);
+    if (!s.d_bar) CK(cudaMalloc(&s.d_bar, 2 * sizeof(unsigned)));
+    ResParams p;
+    std::memset(&p, 0, sizeof p);
+    p.nx = c->nx;
+    p.ny = c->ny;
+    p.nzl = s.nzl;
+    p.nshots = s.nshots;
+    p.plane = (long long)c->nx * c->ny;
+    p.coef[0] = 3.0f * c->coeffs[0];
+    for (int k = 1; k < 6; ++k) p.coef[k] = c->coeffs[k];
+    p.buf0 = s.buf[0];
+    p.buf1 = s.buf[1];
+    p.C = s.C;
+    p.d_step = s.d_step;
+    p.bar = s.d_bar;
+    p.nsrc = (int)s.srcs.size();
+    for (int k = 0; k < p.nsrc; ++k) p.src[k] = s.srcs[k];
+    p.samples = s.d_samples;
+    for (int k = 0; k < nsteps;) {
+        p.parity0 = (int)(c->step & 1);
+        p.nsteps = std::min(nsteps - k, 4096);
+        RET(prof_begin(c, st));
+        CK(launch_resident(p, ctas, tv.TX, st));
+        RET(prof_end(c, st));
+        ++c->launches;
+        c->step += p.nsteps;
+        k += p.nsteps;
+    }
+    return RTM_OK;
+}
+
 int step_single(rtm_ctx* c, int nsteps) {
     Slab& s = c->slabs[0];
     cudaStream_t st = s.stream();
+    if (variant(resolve_tile(c)).kind == 5) return step_resident(c, nsteps);
     int k = 0;
     int tb_bands = 0;
-    if (variant(resolve_tile(c)).kind >= 3) {
+    if (variant(resolve_tile(c)).kind == 4) {
         int tx;
         std::vector<TBBand> b;
         if (tb_plan(c, variant(resolve_tile(c)), &tx, &b)) tb_bands = (int)b.size();

@@ -51,7 +51,8 @@ struct StencilParams {
 struct TileVariant {
     const char* name;
     int kind;                  // 0 naive, 1 k_tiled (CTA per unit), 2 k_stream (persistent, producer
-                               // warp), 4 k_tb2s (two time steps per HBM pass)
+                               // warp), 4 k_tb2s (two time steps per HBM pass),
+                               // 5 k_resident (many steps per launch, L2-resident grids)
     int TX, TY, K, D, MINB;    // tile (x, y), u ring depth, u_prev/C ring depth (0: LDG), min CTAs/SM
     int U;                     // z-loop unroll (register-queue rotation amortised over U planes)
     int KB, DB, L;             // kind 4: KB = W (store groups in flight before publication),
@@ -65,6 +66,11 @@ struct TileVariant {
     X(37, "tb2s_64x16k8d3l24w6u4", 64, 16, 8, 3, 4, 24, 6, 0, 35)         \
     X(38, "tb2s_64x16k8d3l40w6u4", 64, 16, 8, 3, 4, 40, 6, 0, 35)         \
     X(39, "tb2s_64x16k8d3l56w16u4", 64, 16, 8, 3, 4, 56, 16, 0, 35)
+
+// Resident (kind 5) variants: X(id, name, threads, ctas_per_sm, pair)
+#define RTM_RESIDENT_VARIANTS(X)                          \
+    X(40, "resident256x2", 256, 2, 35)                    \
+    X(41, "resident128x4", 128, 4, 35)
 
 // Variant table: index 0 is the naive kernel.
 int num_variants();
@@ -80,6 +86,27 @@ cudaError_t launch_variant(int id, const CUtensorMap* tm_u, const CUtensorMap* t
                            const CUtensorMap* tm_c, const StencilParams& p, int max_ctas,
                            cudaStream_t s);
 cudaError_t launch_naive(const StencilParams& p, cudaStream_t s);
+
+// Resident multi-step kernel (kind 5, k_resident in rtm_resident.cu): nsteps time steps of a
+// single-slab context in one cooperative launch, grid barrier (bar[0..1], zeroed by the
+// launcher) between steps; buffers alternate starting from buf[parity0] = u^n.
+struct ResParams {
+    int nx, ny, nzl, nshots;
+    long long plane;
+    float coef[6];
+    float* buf0;
+    float* buf1;
+    const float* C;
+    int* d_step;
+    int parity0;
+    int nsteps;
+    unsigned* bar;
+    int nsrc;
+    DevSource src[RTM_MAX_SOURCES];
+    const float* samples;
+};
+cudaError_t launch_resident(const ResParams& p, int ctas, int threads, cudaStream_t s);
+cudaError_t resident_occupancy(int threads, int* per_sm);
 
 // Split-role two-step pass (kind 4, k_tb2s in rtm_tb.cu): stage-A and stage-B CTAs of each
 // tile (2 per SM); stage A publishes u^{n+1} planes through TMA stores (flagsA), stage B

@@ -640,6 +640,9 @@ static const TileVariant kVariants[] = {
 #define X(id, name, tx, ty, k, d, u, lmax, w, ch, pair) {name, 4, tx, ty, k, d, 2, u, w, ch, lmax, pair},
     RTM_TB2S_VARIANTS(X)
 #undef X
+#define X(id, name, threads, per_sm, pair) {name, 5, threads, 0, 0, 0, per_sm, 1, 0, 0, 0, pair},
+    RTM_RESIDENT_VARIANTS(X)
+#undef X
 };
 
 int num_variants() { return static_cast<int>(sizeof(kVariants) / sizeof(kVariants[0])); }
@@ -664,6 +667,12 @@ static cudaError_t prepare(const void** fn, int* threads, size_t* smem) {
 
 static cudaError_t variant_fn(int id, const void** fn, int* threads, size_t* smem) {
     if (id > 0 && id < num_variants() && variant(id).kind == 4) return tb2s_variant_fn(id, fn, threads, smem);
+    if (id > 0 && id < num_variants() && variant(id).kind == 5) {
+        *fn = nullptr;
+        *threads = variant(id).TX;
+        *smem = 0;
+        return cudaSuccess;
+    }
     switch (id) {
 #define X(vid, name, kind, tx, ty, k, d, mb, u) \
     case vid:                                   \
@@ -688,6 +697,12 @@ int variant_occupancy(int id, int* threads_per_block) {
     int threads;
     size_t smem;
     if (variant_fn(id, &fn, &threads, &smem) != cudaSuccess) return -1;
+    if (variant(id).kind == 5) {
+        int nb = 0;
+        if (resident_occupancy(threads, &nb) != cudaSuccess) return -1;
+        if (threads_per_block) *threads_per_block = threads;
+        return nb;
+    }
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem) != cudaSuccess)
         return -1;

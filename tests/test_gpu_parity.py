@@ -826,3 +826,44 @@ def test_async_pipeline_batched_shots_and_dist_world1(P):
         P.rtm_read_field_async(sim.h, out)
         P.rtm_sync(sim.h)
         assert np.array_equal(out, ref1)
+
+
+# ----------------------------------------------------------------------------- resident multi-step kernel
+def test_resident_kernel_c1_and_batched_bitwise(P):
+    """k_resident (many steps per cooperative launch, grid barrier between steps) gives the
+    bits of per-step k_stream launches: C1's full run with its source, odd starts and
+    multi-launch runs, and a 3-shot batch; and stays within the oracle tolerance."""
+    ids = [t for t in range(P.rtm_num_tiles()) if P.rtm_tile_name(t).startswith("resident")]
+    assert ids
+    cfg = ri.make_config(1)
+    v = cfg.velocity()
+    src = cfg.sources()
+    ref = gpu_run(P, v, cfg.dx, cfg.dt, cfg.steps, sources=src, tile=35)
+    orc = oracle.run(v, cfg.dx, cfg.dt, C32, cfg.steps, sources=src)
+    for t in ids:
+        with P.Simulation(64, 64, 64, cfg.dx, cfg.dt, C32) as sim:
+            sim.set_tile(t)
+            sim.set_velocity(v)
+            for s in src:
+                sim.inject_source(*s)
+            for k in (1, 40, 3, 56):   # odd start, several launches
+                sim.step(k)
+            got = sim.read_field()
+        assert np.array_equal(got, ref), P.rtm_tile_name(t)
+    assert relerr(got, orc) <= TOL_FULL
+    nz, ny, nx = 18, 22, 36
+    rng = np.random.default_rng(5)
+    vb = rng.uniform(1500, 4300, (nz, ny, nx)).astype(np.float32)
+    u0, up0 = ri.random_fields((3, nz, ny, nx), seed=6)
+    w = ri.source_samples(3000.0, 1e-3, 15.0, 9)
+    outs = []
+    for t in (35, ids[0]):
+        with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, shots=3) as sim:
+            sim.set_tile(t)
+            sim.set_velocity(vb)
+            P.rtm_inject_source_shot(sim.h, 2, 35, 21, 17, w)
+            P.rtm_inject_source_shot(sim.h, 0, 0, 0, 0, -w)
+            sim.set_fields(u0, up0)
+            sim.step(9)
+            outs.append(sim.read_fields())
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
