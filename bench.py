@@ -265,8 +265,11 @@ def main():
         # the paper's two-phase blocksize selection, GPU analogue: every
         # stream-kernel variant timed on this grid (max over ranks = MWMB), winner verified
         P.rtm_set_velocity_device(h, d_v.data_ptr())
-        cands = [t for t in range(P.rtm_num_tiles())
-                 if (P.rtm_tile_name(t) or "").startswith(("stream", "tb2", "resident"))]
+        # two-step passes need a single-slab single-shot context and the resident kernel a
+        # single slab; elsewhere they would run their paired k_stream variant
+        kinds = ("stream",) + (("resident",) if world == 1 else ()) + \
+            (("tb2",) if world == 1 and args.shots == 1 else ())
+        cands = [t for t in range(P.rtm_num_tiles()) if (P.rtm_tile_name(t) or "").startswith(kinds)]
         res, times = P.rtm_autotune(h, args.tune_ni, tiles=cands)
         tune = {"selected": P.rtm_tile_name(res["best_tile"]), "candidates": len(cands),
                 "nI": args.tune_ni, "min_time_ms": round(res["min_time_ms"], 4),
