@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--halo", type=int, default=0, choices=[0, 2],
                     help="N > 1 halo exchange: 0 NCCL send/recv (default), 2 fused push over "
                          "CUDA-IPC peer stores + flag protocol (SURVEY §8(f) f1)")
+    ap.add_argument("--pdl", type=int, default=-1, choices=[-1, 0, 1],
+                    help="programmatic dependent launch of consecutive steps (-1: library default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="short run for ncu captures (no extras)")
@@ -244,6 +246,8 @@ def main():
     else:
         z0, nzl = 0, cfg.nz
         h = P.rtm_create(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32)
+    if args.pdl != -1:
+        P.rtm_set_option(h, P.RTM_OPT_PDL, args.pdl)
     if args.tile != -1:
         P.rtm_set_tile(h, args.tile)
     if args.zchunk:

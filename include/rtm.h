@@ -177,9 +177,12 @@ const char* rtm_tile_name(int tile_id);  /* e.g. "stream64x32k10d0"; NULL for un
  *   RTM_OPT_TB_CTAS    two-step variants ("tb2_*"): max CTAs per y-band launch,
  *                      0 (default) = one per SM.  Smaller values force more, narrower bands
  *                      (used by the tests to cover band edges on small grids).
+ *   RTM_OPT_PDL        1: launch consecutive k_stream steps with programmatic dependent launch
+ *                      (the next step's CTAs are scheduled while the previous grid drains and
+ *                      wait on griddepcontrol.wait before touching memory); 0: plain launches.
  * Unknown key or out-of-range value -> RTM_EINVAL.  rtm_get_option returns -1 for unknown keys. */
 enum { RTM_OPT_ZCHUNK = 1, RTM_OPT_CACHE_MODE = 2, RTM_OPT_GRAPHS = 3, RTM_OPT_SHOT_ORDER = 4,
-       RTM_OPT_HALO_MODE = 5, RTM_OPT_CHECK_EVERY = 6, RTM_OPT_TB_CTAS = 7 };
+       RTM_OPT_HALO_MODE = 5, RTM_OPT_CHECK_EVERY = 6, RTM_OPT_TB_CTAS = 7, RTM_OPT_PDL = 8 };
 int rtm_set_option(rtm_ctx* ctx, int key, long long value);
 long long rtm_get_option(rtm_ctx* ctx, int key);
 

@@ -143,6 +143,7 @@ struct rtm_ctx {
     unsigned sig_flush = 0;          // CU_STREAM_WAIT_VALUE_FLUSH when the devices support it
     int check_every = 0;    // NaN/Inf scan every k steps (0 = off)
     int tb_ctas = 0;        // two-step passes: max CTAs per band (0 = #SMs)
+    bool pdl = false;       // programmatic dependent launch of consecutive k_stream steps
     int l2_bytes = 0;
     bool graphs = true;
     std::vector<HostSource> sources;
@@ -480,7 +481,7 @@ int launch_stencil(rtm_ctx* c, Slab& s, int parity, int b0, int l0, int b1, int 
         p.r_chunks[0] = choose_chunks(c, s.occupancy, nt * s.nshots, l0);  // units = tiles x chunks x shots
         p.r_chunks[1] = l1 > 0 ? choose_chunks(c, s.occupancy, nt * s.nshots, l1) : 0;
         CK(launch_variant(var, &s.tm_u[parity], &s.tm_in[parity ^ 1], &s.tm_c, p,
-                          c->num_sms * s.occupancy, st));
+                          c->num_sms * s.occupancy, st, c->pdl && variant(var).kind == 2));
     }
     if (c->profiling) {
         CK(cudaEventRecord(e1, st));
@@ -1686,6 +1687,10 @@ int rtm_set_option(rtm_ctx* c, int key, long long value) {
             if (value < 0 || value > (1 << 20)) return fail(RTM_EINVAL, "tb ctas %lld out of range", value);
             c->tb_ctas = (int)value;
             break;
+        case RTM_OPT_PDL:
+            if (value < 0 || value > 1) return fail(RTM_EINVAL, "pdl %lld not in 0..1", value);
+            c->pdl = value != 0;
+            break;
         case RTM_OPT_HALO_MODE:
             if (value < 0 || value > 2) return fail(RTM_EINVAL, "halo mode %lld not in 0..2", value);
             if (value == 1 && c->mode != 1)
@@ -1728,6 +1733,7 @@ long long rtm_get_option(rtm_ctx* c, int key) {
         case RTM_OPT_HALO_MODE: return c->halo_mode;
         case RTM_OPT_CHECK_EVERY: return c->check_every;
         case RTM_OPT_TB_CTAS: return c->tb_ctas;
+        case RTM_OPT_PDL: return c->pdl ? 1 : 0;
         default: return -1;
     }
 }

@@ -82,9 +82,11 @@ int variant_occupancy(int id, int* threads_per_block);
 
 // tm_u: u^n with the (TX+16) x (TY+10) halo box; tm_up: u^{n-1} and tm_c: C with TX x TY
 // boxes (k_stream with D > 0).  max_ctas bounds the persistent grid.
+// pdl: programmatic dependent launch (k_stream only): the grid may be scheduled while the
+// previous kernel on the stream drains; it waits (griddepcontrol.wait) before touching memory.
 cudaError_t launch_variant(int id, const CUtensorMap* tm_u, const CUtensorMap* tm_up,
                            const CUtensorMap* tm_c, const StencilParams& p, int max_ctas,
-                           cudaStream_t s);
+                           cudaStream_t s, bool pdl = false);
 cudaError_t launch_naive(const StencilParams& p, cudaStream_t s);
 
 // Resident multi-step kernel (kind 5, k_resident in rtm_resident.cu): nsteps time steps of a

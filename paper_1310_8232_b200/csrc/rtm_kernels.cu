@@ -376,9 +376,14 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
         }
         fence_mbar_init();
     }
+    __syncthreads();
+    // Programmatic dependent launch: everything above overlapped the previous grid's tail;
+    // every global access below depends on it (u, u_prev, the step counter), so wait for its
+    // completion here (a no-op for a normal launch), then let the next grid be scheduled.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (p.write_next && blockIdx.x == 0 && tid == 0)
         p.d_step[p.parity ^ 1] = p.d_step[p.parity] + 1;
-    __syncthreads();
 
     const int units = p.tiles_x * p.tiles_y * (p.r_chunks[0] + (p.nranges > 1 ? p.r_chunks[1] : 0)) *
                       p.nshots;
@@ -712,7 +717,7 @@ int variant_occupancy(int id, int* threads_per_block) {
 
 cudaError_t launch_variant(int id, const CUtensorMap* tm_u, const CUtensorMap* tm_up,
                            const CUtensorMap* tm_c, const StencilParams& p, int max_ctas,
-                           cudaStream_t s) {
+                           cudaStream_t s, bool pdl) {
     const void* fn;
     int threads;
     size_t smem;
@@ -729,7 +734,18 @@ cudaError_t launch_variant(int id, const CUtensorMap* tm_u, const CUtensorMap* t
     const long long grid = units < max_ctas ? units : max_ctas;
     void* args[] = {const_cast<CUtensorMap*>(tm_u), const_cast<CUtensorMap*>(tm_up),
                     const_cast<CUtensorMap*>(tm_c), const_cast<StencilParams*>(&p)};
-    return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(threads), args, smem, s);
+    if (!pdl) return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(threads), args, smem, s);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 cudaError_t launch_naive(const StencilParams& p, cudaStream_t s) {

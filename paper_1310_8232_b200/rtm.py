@@ -21,6 +21,7 @@ RTM_MAX_SOURCES = 64
 RTM_OPT_ZCHUNK, RTM_OPT_CACHE_MODE, RTM_OPT_GRAPHS, RTM_OPT_SHOT_ORDER, RTM_OPT_HALO_MODE = 1, 2, 3, 4, 5
 RTM_OPT_CHECK_EVERY = 6
 RTM_OPT_TB_CTAS = 7
+RTM_OPT_PDL = 8
 _NAMES = {0: "RTM_OK", -1: "RTM_EINVAL", -2: "RTM_ECFL", -3: "RTM_ENOMEM", -4: "RTM_ECUDA",
           -5: "RTM_ENCCL", -6: "RTM_ESTATE", -7: "RTM_EUNSTABLE"}
 

@@ -867,3 +867,25 @@ def test_resident_kernel_c1_and_batched_bitwise(P):
             sim.step(9)
             outs.append(sim.read_fields())
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_pdl_launches_bitwise(P):
+    """Programmatic dependent launch of consecutive k_stream steps (graph and direct paths,
+    multi-slab fused mode) gives the same bits as plain launches."""
+    cfg = ri.make_config(2, shape=(48, 40, 64), steps=37)
+    v = cfg.velocity()
+    src = cfg.sources()
+    ref = gpu_run(P, v, cfg.dx, cfg.dt, 37, sources=src, tile=35)
+    for devices, halo in ((None, 0), ([0, 0, 0], 2), ([0, 0], 1)):
+        with P.Simulation(64, 40, 48, cfg.dx, cfg.dt, C32, devices=devices) as sim:
+            P.rtm_set_option(sim.h, P.RTM_OPT_PDL, 1)
+            assert P.rtm_get_option(sim.h, P.RTM_OPT_PDL) == 1
+            if halo:
+                P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, halo)
+            sim.set_tile(35)
+            sim.set_velocity(v)
+            for s in src:
+                sim.inject_source(*s)
+            sim.step(3)
+            sim.step(34)
+            assert np.array_equal(sim.read_field(), ref), (devices, halo)
