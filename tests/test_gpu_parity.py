@@ -889,3 +889,40 @@ def test_pdl_launches_bitwise(P):
             sim.step(3)
             sim.step(34)
             assert np.array_equal(sim.read_field(), ref), (devices, halo)
+
+
+def test_new_paths_edge_cases(P):
+    """Asynchronous calls refuse multi-slab contexts; the two-step and resident variants run
+    under the field check and under per-launch profiling; option ranges are validated."""
+    nz, ny, nx = 24, 30, 64
+    v = np.full((nz, ny, nx), 2500.0, np.float32)
+    u0, up0 = ri.random_fields(v.shape, seed=31)
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, devices=[0, 0]) as sim:
+        sim.set_velocity(v)
+        for call in (lambda: P.rtm_set_velocity_async(sim.h, v), lambda: P.rtm_step_async(sim.h, 1),
+                     lambda: P.rtm_read_field_async(sim.h, np.empty(v.shape, np.float32))):
+            with pytest.raises(P.RtmError) as e:
+                call()
+            assert e.value.code == P.RTM_EINVAL
+    ref = gpu_run(P, v, 10.0, 1e-3, 12, u0=u0, up0=up0, tile=35)
+    names = {P.rtm_tile_name(t): t for t in range(P.rtm_num_tiles())}
+    for name in [n for n in names if n.startswith(("tb2s_", "resident"))][:2] + ["resident256x2"]:
+        for mode in ("check", "profile"):
+            with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32) as sim:
+                sim.set_tile(names[name])
+                sim.set_velocity(v)
+                sim.set_fields(u0, up0)
+                if mode == "check":
+                    P.rtm_set_option(sim.h, P.RTM_OPT_CHECK_EVERY, 5)
+                else:
+                    P.rtm_set_profiling(sim.h, 1)
+                sim.step(7)
+                sim.step(5)
+                if mode == "profile":
+                    launches, ms = P.rtm_kernel_stats(sim.h)
+                    assert launches >= 1 and ms > 0
+                assert np.array_equal(sim.read_field(), ref), (name, mode)
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32) as sim:
+        for key, bad in ((P.RTM_OPT_PDL, 2), (P.RTM_OPT_TB_CTAS, -1), (P.RTM_OPT_HALO_MODE, 3)):
+            with pytest.raises(P.RtmError):
+                P.rtm_set_option(sim.h, key, bad)
