@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--tile", type=int, default=-1,
                     help="kernel variant; -1 = choose with rtm_autotune (untimed, before warm-up)")
     ap.add_argument("--tune-ni", type=int, default=4, help="autotune iterations per candidate")
+    ap.add_argument("--lattice", type=int, default=0,
+                    help="P > 1: autotune over the stream tiles x the paper's P-parts z-chunk "
+                         "lattice (PAPER.md:296-301); 0: automatic z-chunk per tile")
     ap.add_argument("--zchunk", type=int, default=0)
     ap.add_argument("--nsteps", type=int, default=0, help="override the config's time steps")
     ap.add_argument("--shots", type=int, default=1,
@@ -274,9 +277,14 @@ def main():
         kinds = ("stream",) + (("resident",) if world == 1 else ()) + \
             (("tb2",) if world == 1 and args.shots == 1 else ())
         cands = [t for t in range(P.rtm_num_tiles()) if (P.rtm_tile_name(t) or "").startswith(kinds)]
-        res, times = P.rtm_autotune(h, args.tune_ni, tiles=cands)
+        zcs = None
+        if args.lattice > 1:  # the paper's nC = |tiles| x |b_z| candidates (selection phase)
+            lat = P.rtm_blocksize_lattice(nzl, args.lattice)
+            cands, zcs = [t for t in cands for _ in lat], [z for _ in cands for z in lat]
+        res, times = P.rtm_autotune(h, args.tune_ni, tiles=cands, zchunks=zcs)
         tune = {"selected": P.rtm_tile_name(res["best_tile"]), "candidates": len(cands),
                 "nI": args.tune_ni, "min_time_ms": round(res["min_time_ms"], 4),
+                "zchunk": res.get("best_zchunk"), "lattice_P": args.lattice or None,
                 "actual_time_ms": round(res["actual_time_ms"], 4),
                 "quality_pct": round(res["quality_pct"], 2)}
 

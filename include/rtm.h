@@ -224,6 +224,17 @@ typedef struct {
 } rtm_tune_result;
 int rtm_autotune(rtm_ctx* ctx, int nI, const int* tiles, const int* zchunks, int ncand,
                  rtm_tune_result* out, double* cand_ms);
+/* The paper's candidate lattice for one dimension ("divided in P parts"):
+ * b = < 1, S/(P-1) + 1, 2S/(P-1) + 1, ..., (P-1)S/(P-1) + 1 >, integer division, each value
+ * clamped to [1, S] (the worked example at PAPER.md:301 lists 200 for S = 200, P = 5: the
+ * formula's last term S+1 is read as S, R17) and duplicates (small S) removed.
+ * Writes at most P values to out (ascending) and returns their count; P < 2 or S < 1 ->
+ * RTM_EINVAL.  Host-only (no device).  On the GPU the runtime blocksize dimension is the
+ * z-chunk length of a work unit (the xy block is the compile-time tile of a variant), so
+ * rtm_autotune over {tiles} x rtm_blocksize_lattice(nz, P) is the paper's nC-candidate
+ * selection phase. */
+int rtm_blocksize_lattice(int S, int P, int* out);
+
 /* MWMB selection (host-only): times[r*ncand + c] = time of candidate c on rank r; returns the
  * c minimising max_r times[r][c] (ties -> lowest c), or -1 on invalid input. */
 int rtm_select_mwmb(const double* times, int nranks, int ncand);

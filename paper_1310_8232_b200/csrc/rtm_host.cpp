@@ -1738,6 +1738,17 @@ long long rtm_get_option(rtm_ctx* c, int key) {
     }
 }
 
+int rtm_blocksize_lattice(int S, int P, int* out) {
+    if (S < 1 || P < 2 || !out) return fail(RTM_EINVAL, "lattice needs S >= 1, P >= 2, out != NULL");
+    int n = 0;
+    for (int k = 0; k < P; ++k) {
+        long long b = (long long)k * S / (P - 1) + 1;
+        if (b > S) b = S;                               // PAPER.md:301 worked example (R17)
+        if (n == 0 || out[n - 1] != (int)b) out[n++] = (int)b;
+    }
+    return n;
+}
+
 int rtm_select_mwmb(const double* times, int nranks, int ncand) {
     if (!times || nranks < 1 || ncand < 1) return -1;
     int best = -1;

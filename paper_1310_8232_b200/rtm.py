@@ -83,6 +83,7 @@ _SIGS = {
     "rtm_nu_crit": (_D, [_P]),
     "rtm_autotune": (_I, [_P, _I, _P, _P, _I, ctypes.POINTER(rtm_tune_result), _P]),
     "rtm_select_mwmb": (_I, [_P, _I, _I]),
+    "rtm_blocksize_lattice": (_I, [_I, _I, _P]),
     "rtm_set_velocity_async": (_I, [_P, _P]),
     "rtm_step_async": (_I, [_P, _I]),
     "rtm_read_field_async": (_I, [_P, _P]),
@@ -197,6 +198,15 @@ def _async_buf(a, name, write=False):
         raise ValueError(f"{name} must be a C-contiguous float32 array"
                          + (" (writeable)" if write else ""))
     return _ptr(a)
+
+
+def rtm_blocksize_lattice(S, P) -> list[int]:
+    """PAPER.md:296-301 candidate values for one dimension of size S divided in P parts."""
+    out = (_I * max(int(P), 1))()
+    n = lib.rtm_blocksize_lattice(int(S), int(P), out)
+    if n < 0:
+        raise RtmError(n, _err())
+    return [int(out[k]) for k in range(n)]
 
 
 def rtm_set_velocity_async(h, v):

@@ -171,3 +171,20 @@ def test_bench_reference_arm_contract():
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["unit"] == d["unit"]
+
+
+def test_blocksize_lattice_paper_worked_example(P):
+    """PAPER.md:301: for 200x200x800 and P = 5, b_i = b_j = <1, 51, 101, 151, 200> and
+    b_k = <1, 201, 401, 601, 800>, nC = 125; P = 10 / 20 give nC = 1000 / 8000."""
+    assert P.rtm_blocksize_lattice(200, 5) == [1, 51, 101, 151, 200]
+    assert P.rtm_blocksize_lattice(800, 5) == [1, 201, 401, 601, 800]
+    for parts, nc in ((5, 125), (10, 1000), (20, 8000)):
+        dims = [P.rtm_blocksize_lattice(s, parts) for s in (200, 200, 800)]
+        assert all(len(b) == parts for b in dims)
+        assert len(dims[0]) * len(dims[1]) * len(dims[2]) == nc
+        for s, b in zip((200, 200, 800), dims):
+            assert b[0] == 1 and b[-1] == s and b == sorted(set(b)) and all(1 <= x <= s for x in b)
+    assert P.rtm_blocksize_lattice(3, 10) == [1, 2, 3]  # duplicates of a small S collapse
+    for bad in ((0, 5), (10, 1)):
+        with pytest.raises(P.RtmError):
+            P.rtm_blocksize_lattice(*bad)

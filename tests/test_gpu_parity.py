@@ -926,3 +926,28 @@ def test_new_paths_edge_cases(P):
         for key, bad in ((P.RTM_OPT_PDL, 2), (P.RTM_OPT_TB_CTAS, -1), (P.RTM_OPT_HALO_MODE, 3)):
             with pytest.raises(P.RtmError):
                 P.rtm_set_option(sim.h, key, bad)
+
+
+def test_autotune_over_paper_lattice_is_exhaustive_argmin(P):
+    """Selection phase over {2 tiles} x the P-parts z-chunk lattice: the
+    installed candidate is the argmin of the per-candidate times (the exhaustive-lattice
+    ranking, MWMB at one rank), the verification time is reported, the wavefield is kept."""
+    nz, ny, nx = 40, 48, 64
+    v = np.full((nz, ny, nx), 2500.0, np.float32)
+    u0, up0 = ri.random_fields(v.shape, seed=8)
+    lat = P.rtm_blocksize_lattice(nz, 4)
+    assert lat == [1, 14, 27, 40]
+    tiles = [1, 35]
+    cands = [t for t in tiles for _ in lat]
+    zcs = [z for _ in tiles for z in lat]
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32) as sim:
+        sim.set_velocity(v)
+        sim.set_fields(u0, up0)
+        res, times = P.rtm_autotune(sim.h, 3, tiles=cands, zchunks=zcs)
+        k = int(np.argmin(times))
+        assert len(times) == len(cands) and np.all(times > 0)
+        assert (res["best_tile"], res["best_zchunk"]) == (cands[k], zcs[k])
+        assert res["actual_time_ms"] > 0
+        assert sim.tile == cands[k] and P.rtm_get_option(sim.h, P.RTM_OPT_ZCHUNK) == zcs[k]
+        u, up = sim.read_fields()
+        assert np.array_equal(u, u0) and np.array_equal(up, up0)
