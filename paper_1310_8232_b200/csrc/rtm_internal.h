@@ -70,7 +70,8 @@ struct TileVariant {
 // Resident (kind 5) variants: X(id, name, threads, ctas_per_sm, pair)
 #define RTM_RESIDENT_VARIANTS(X)                          \
     X(40, "resident256x2", 256, 2, 35)                    \
-    X(41, "resident128x4", 128, 4, 35)
+    X(41, "resident128x4", 128, 4, 35)                    \
+    X(42, "resident512x1", 512, 1, 35)
 
 // Variant table: index 0 is the naive kernel.
 int num_variants();
@@ -102,7 +103,7 @@ struct ResParams {
     int* d_step;
     int parity0;
     int nsteps;
-    unsigned* bar;
+    unsigned* bar;             // [2]: grid barrier arrival counter (zeroed per launch), spare
     int nsrc;
     DevSource src[RTM_MAX_SOURCES];
     const float* samples;

@@ -24,34 +24,32 @@ __device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
     return v;
 }
 
-// Sense-free grid barrier on bar[0] (arrivals) / bar[1] (generation), zeroed before the launch.
+// Grid barrier on a monotonically increasing arrival counter bar[0] (zeroed before the launch):
+// barrier k of the launch is passed when bar[0] >= (k+1) * gridDim.x.  One release-add per CTA
+// (its stores of the step happen-before the arrival) and acquire-polling; no reset and no
+// generation flip by the last arriver (one L2 round trip less than a sense-reversing barrier).
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();  // this CTA's stores of the step, before its arrival
-        const unsigned g = gen;
-        if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
-            bar[0] = 0;
-            __threadfence();
-            atomicExch(&bar[1], g + 1);
-        } else {
-            unsigned long long t0 = 0;
-            unsigned spins = 0;
-            while (ld_acquire_gpu_u32(&bar[1]) == g) {
-                if ((++spins & 255) == 0) {
-                    unsigned long long t;
-                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-                    if (!t0) t0 = t;
-                    else if (t - t0 > 4000000000ull) __trap();  // watchdog: error, never a hang
-                }
+        const unsigned target = (gen + 1) * gridDim.x;
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        unsigned long long t0 = 0;
+        unsigned spins = 0;
+        while (ld_acquire_gpu_u32(bar) < target) {
+            if ((++spins & 255) == 0) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                if (!t0) t0 = t;
+                else if (t - t0 > 4000000000ull) __trap();  // watchdog: error, never a hang
             }
         }
-        gen = g + 1;
     }
+    ++gen;
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) k_resident(const __grid_constant__ ResParams p) {
+template <int NT>
+__global__ void __launch_bounds__(NT) k_resident(const __grid_constant__ ResParams p) {
     const float c[6] = {p.coef[0], p.coef[1], p.coef[2], p.coef[3], p.coef[4], p.coef[5]};
     const int nxq = p.nx >> 2;
     const long long per_shot = (long long)p.nzl * p.ny * nxq;
@@ -116,8 +114,19 @@ __global__ void __launch_bounds__(256) k_resident(const __grid_constant__ ResPar
     if (blockIdx.x == 0 && threadIdx.x == 0) p.d_step[(p.parity0 + p.nsteps) & 1] = n0 + p.nsteps;
 }
 
+static const void* resident_fn(int threads) {
+    switch (threads) {
+        case 128: return reinterpret_cast<const void*>(&k_resident<128>);
+        case 256: return reinterpret_cast<const void*>(&k_resident<256>);
+        case 512: return reinterpret_cast<const void*>(&k_resident<512>);
+        default: return nullptr;
+    }
+}
+
 cudaError_t resident_occupancy(int threads, int* per_sm) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_resident, threads, 0);
+    const void* fn = resident_fn(threads);
+    if (!fn) return cudaErrorInvalidValue;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, fn, threads, 0);
 }
 
 cudaError_t launch_resident(const ResParams& p, int ctas, int threads, cudaStream_t s) {
@@ -134,7 +143,9 @@ cudaError_t launch_resident(const ResParams& p, int ctas, int threads, cudaStrea
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(&k_resident), args);
+    const void* fn = resident_fn(threads);
+    if (!fn) return cudaErrorInvalidValue;
+    return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 }  // namespace rtm
