@@ -951,3 +951,27 @@ def test_autotune_over_paper_lattice_is_exhaustive_argmin(P):
         assert sim.tile == cands[k] and P.rtm_get_option(sim.h, P.RTM_OPT_ZCHUNK) == zcs[k]
         u, up = sim.read_fields()
         assert np.array_equal(u, u0) and np.array_equal(up, up0)
+
+
+def test_beyond_2pow32_points_one_step_sampled(P):
+    """A 2048 x 2048 x 1024 grid (4.3e9 points > 2^32, 52 GB of fields on the device): every
+    offset is 64-bit.  One step from random ICs with the default (autotune-free) variant,
+    sampled against the oracle point evaluator, with samples forced into the last planes,
+    rows and columns."""
+    nz, ny, nx = 1024, 2048, 2048
+    v = ri.layered_velocity((nz, ny, nx), np.array([1800, 2600, 3200, 3900, 4200, 2900], np.float32))
+    u0, up0 = ri.random_fields(v.shape, seed=4242)
+    with P.Simulation(nx, ny, nz, 10.0, 0.8e-3, C32) as sim:
+        sim.set_velocity(v)
+        sim.set_fields(u0, up0)
+        sim.step(1)
+        got = sim.read_field()
+    rng = np.random.default_rng(4243)
+    m = 60_000
+    pts = np.stack([rng.integers(0, nx, m), rng.integers(0, ny, m), rng.integers(0, nz, m)], 1)
+    tail = np.stack([rng.integers(0, nx, 4000), rng.integers(ny - 8, ny, 4000),
+                     rng.integers(nz - 8, nz, 4000)], 1)
+    edge = np.array([[nx - 1, ny - 1, nz - 1], [0, 0, 0], [nx - 1, 0, nz - 1], [0, ny - 1, nz - 2]])
+    pts = np.concatenate([pts, tail, edge]).astype(np.int32)
+    ref = oracle.points_f32(v, 10.0, 0.8e-3, C32, u0, up0, pts)
+    assert relerr(got[pts[:, 2], pts[:, 1], pts[:, 0]], ref) <= TOL_1
