@@ -183,11 +183,28 @@ def run_reference(args):
             "config": {"workload": f"C{cfg.k}", "grid": [cfg.nx, cfg.ny, cfg.nz],
                        "time_steps": cfg.steps, "sample": sample},
             "cpu_baseline": {"value": round(val, 4), "unit": "Gpoints/s", "cores": cores,
-                             "kind": "oracle", "sample": sample},
+                             "kind": "oracle", "sample": sample,
+                             "cpu_model": host_cpu()[0], "sockets": host_cpu()[1]},
             "e2e": {"value": round(val, 4), "unit": "Gpoints/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def host_cpu():
+    """(model name, sockets) of the host from /proc/cpuinfo (state the CPU)."""
+    model, sockets = None, set()
+    try:
+        for line in open("/proc/cpuinfo"):
+            k, _, val = line.partition(":")
+            k = k.strip()
+            if k == "model name" and model is None:
+                model = val.strip()
+            elif k == "physical id":
+                sockets.add(val.strip())
+    except OSError:
+        pass
+    return model, (len(sockets) or None)
 
 
 def cpu_baseline(cfg, v_full):
@@ -208,7 +225,9 @@ def cpu_baseline(cfg, v_full):
     oracle.run(v, cfg.dx, cfg.dt, ri.COEFFS_F32, n, nthreads=cores)
     dt = time.perf_counter() - t
     val = v.size * n / dt / 1e9
+    model, sockets = host_cpu()
     return {"value": round(val, 4), "unit": "Gpoints/s", "cores": cores, "kind": "oracle",
+            "cpu_model": model, "sockets": sockets,
             "sample": f"first {planes} z-planes of C{cfg.k} ({cfg.nx}x{cfg.ny}x{planes}), "
                       f"{n} time steps, {dt:.1f} s"}
 
