@@ -54,8 +54,10 @@ enum {
 
 /* Create a single-GPU context on the current CUDA device for an nx*ny*nz interior grid.
  * dx > 0 (m), dt > 0 (s) finite; coeffs[0..5] = c0..c5 finite, with S_max > 0 (a valid
- * negative-definite 2nd difference).  Allocates u, u_prev (each nx*ny*(nz+10) floats:
- * 5 explicit zero z-halo planes per side) and C (nx*ny*nz floats), zero-initialised.
+ * negative-definite 2nd difference).  Allocates u, u_prev (each px*ny*(nz+10) floats:
+ * 5 explicit zero z-halo planes per side) and C (px*ny*nz floats), zero-initialised, where
+ * px = nx rounded up to a multiple of 4 is the device row pitch (any nx >= 1 runs every
+ * kernel; the padding columns stay zero; host arrays are always unpadded, nx per row).
  * Returns NULL on error (see rtm_last_error()). */
 rtm_ctx* rtm_create(int nx, int ny, int nz, float dx, float dt, const float coeffs[6]);
 
@@ -275,7 +277,8 @@ rtm_ctx* rtm_create_dist(int nx, int ny, int nz_global, float dx, float dt,
  * rtm_slab_range: rank's owned global planes [*z0, *z0 + *nzl); balanced split
  *   z0 = rank*nz/world (floor).  RTM_EINVAL if world < 1, rank out of range, or a slab
  *   would have fewer than 10 planes when world > 1.
- * rtm_halo_plan: element offsets, within a slab buffer of nx*ny*(nzl+10) floats, of
+ * rtm_halo_plan: element offsets, within a slab buffer of nx*ny*(nzl+10) floats (pass the
+ *   row pitch as nx for the device layout), of
  *   [0] send_lo  (owned planes 0..4   -> rank-1),  [1] recv_lo (halo planes -5..-1),
  *   [2] send_hi  (owned planes nzl-5.. -> rank+1), [3] recv_hi (halo planes nzl..nzl+4);
  *   *count = 5*nx*ny elements per message; an offset is -1 when that neighbour is absent. */

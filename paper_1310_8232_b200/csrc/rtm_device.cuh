@@ -196,6 +196,17 @@ __device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* t
         : "memory");
 }
 
+// Rows are pitched to a multiple of 4 floats; the padding columns x >= nx must stay zero (they
+// are the Dirichlet x-halo for every load that reaches them), so a 4-point group that straddles
+// nx stores zeros in its padding lanes.
+__device__ __forceinline__ void zero_pad(float (&out)[4], int x, int nx) {
+    if (x + 4 > nx) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (x + k >= nx) out[k] = 0.0f;
+    }
+}
+
 // The k_stream per-thread update of 4 x-consecutive points, split into the operand gather
 // (from shared memory in k_stream / k_tb2s, from L2 in k_resident) and ONE arithmetic core, so
 // every kernel performs the same operations in the same order (bitwise-identical results).

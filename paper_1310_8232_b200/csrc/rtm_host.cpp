@@ -124,6 +124,7 @@ struct Slab {
 struct rtm_ctx {
     int mode = 0;  // 0 single, 1 multi (in-process slabs), 2 dist (NCCL)
     int nx = 0, ny = 0, nz = 0;  // nz = global planes
+    int px = 0;                  // device row pitch in floats: nx rounded up to a multiple of 4
     float dx = 0, dt = 0;
     float coeffs[6] = {};
     double nu_crit = 0;
@@ -234,9 +235,13 @@ int validate_grid(int nx, int ny, int nz, float dx, float dt, const float* coeff
     return RTM_OK;
 }
 
+// Device planes are pitched (c->px floats per row); host arrays are unpadded (nx per row).
+size_t dplane(const rtm_ctx* c) { return (size_t)c->px * c->ny; }
+size_t hplane(const rtm_ctx* c) { return (size_t)c->nx * c->ny; }
+
 int alloc_slab(rtm_ctx* c, Slab& s) {
     CK(cudaSetDevice(s.dev));
-    const size_t plane = (size_t)c->nx * c->ny;
+    const size_t plane = dplane(c);
     const size_t nbuf = plane * s.buf_planes();
     for (int b = 0; b < 2; ++b) {
         if (cudaMalloc(&s.buf[b], nbuf * sizeof(float)) != cudaSuccess) {
@@ -327,6 +332,7 @@ rtm_ctx* new_ctx(int nx, int ny, int nz, float dx, float dt, const float* coeffs
     }
     rtm_ctx* c = new rtm_ctx();
     c->nx = nx;
+    c->px = (nx + 3) / 4 * 4;
     c->ny = ny;
     c->nz = nz;
     c->dx = dx;
@@ -347,7 +353,6 @@ int finish_ctx(rtm_ctx* c) {
 }
 
 int resolve_tile(const rtm_ctx* c) {
-    if (c->nx % 4 != 0) return 0;  // 128-bit rows / TMA strides need nx % 4 == 0
     if (c->tile >= 0) return c->tile;
     return 35;  // stream64x30k10d6u4: best on C4 (profiles/sweep_c4_s6.log); bench autotunes
 }
@@ -359,12 +364,14 @@ int single_variant(const rtm_ctx* c) {
     return variant(v).kind >= 3 ? variant(v).pair : v;
 }
 
-int encode_3d(CUtensorMap* tm, void* base, int nx, int ny, int nplanes, int bx, int by,
+// 3D tensor map over a pitched device field: logical x extent nx (TMA zero-fills x >= nx, so
+// the padding columns are never read through it), row stride px floats.
+int encode_3d(CUtensorMap* tm, void* base, const rtm_ctx* c, int nplanes, int bx, int by,
               int promo = 3) {
     auto enc = encode_fn();
     if (!enc) return fail(RTM_ECUDA, "cuTensorMapEncodeTiled unavailable from the driver");
-    cuuint64_t dims[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nplanes};
-    cuuint64_t strides[2] = {(cuuint64_t)nx * 4, (cuuint64_t)nx * ny * 4};
+    cuuint64_t dims[3] = {(cuuint64_t)c->nx, (cuuint64_t)c->ny, (cuuint64_t)nplanes};
+    cuuint64_t strides[2] = {(cuuint64_t)c->px * 4, (cuuint64_t)c->px * c->ny * 4};
     cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
     cuuint32_t es[3] = {1, 1, 1};
     CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es,
@@ -386,11 +393,11 @@ int ensure_tmaps(rtm_ctx* c, Slab& s, int var) {
     if (var == 0 || s.tm_variant == key) return RTM_OK;
     const TileVariant& tv = variant(var);
     for (int b = 0; b < 2; ++b) {
-        RET(encode_3d(&s.tm_u[b], s.buf[b], c->nx, c->ny, (int)s.buf_planes(), tv.TX + 16,
+        RET(encode_3d(&s.tm_u[b], s.buf[b], c, (int)s.buf_planes(), tv.TX + 16,
                       tv.TY + 10, promo));
-        RET(encode_3d(&s.tm_in[b], s.buf[b], c->nx, c->ny, (int)s.buf_planes(), tv.TX, tv.TY));
+        RET(encode_3d(&s.tm_in[b], s.buf[b], c, (int)s.buf_planes(), tv.TX, tv.TY));
     }
-    RET(encode_3d(&s.tm_c, s.C, c->nx, c->ny, s.nzl, tv.TX, tv.TY));
+    RET(encode_3d(&s.tm_c, s.C, c, s.nzl, tv.TX, tv.TY));
     int tpb = 0;
     s.occupancy = variant_occupancy(var, &tpb);
     if (s.occupancy < 1)
@@ -423,8 +430,9 @@ void fill_params(const rtm_ctx* c, const Slab& s, int parity, StencilParams& p) 
     p.nx = c->nx;
     p.ny = c->ny;
     p.nzl = s.nzl;
+    p.pitch = c->px;
     p.nshots = s.nshots;
-    p.plane = (long long)c->nx * c->ny;
+    p.plane = (long long)dplane(c);
     p.coef[0] = 3.0f * c->coeffs[0];
     for (int k = 1; k < 6; ++k) p.coef[k] = c->coeffs[k];
     p.u = s.buf[parity];
@@ -563,7 +571,7 @@ struct TBBand {
 // + 5 each side, clipped to the grid) must fit the CTA grid tiles_x x tiles_y <= #SMs (one
 // resident CTA per SM).  Rows are split evenly over the fewest bands that fit.
 bool tb_plan(const rtm_ctx* c, const TileVariant& tv, int* tiles_x, std::vector<TBBand>* bands) {
-    if (c->mode != 0 || c->slabs.size() != 1 || c->slabs[0].nshots != 1 || c->nx % 4) return false;
+    if (c->mode != 0 || c->slabs.size() != 1 || c->slabs[0].nshots != 1) return false;
     const int tx = (c->nx + tv.TX - 1) / tv.TX;
     const int ctas = c->tb_ctas > 0 ? std::min(c->tb_ctas, c->num_sms) : c->num_sms;
     const int cap = ctas / tx;  // tile rows per band
@@ -600,7 +608,7 @@ bool tb_active(const rtm_ctx* c) {
 int tb_alloc(rtm_ctx* c, Slab& s) {
     if (s.alt[0]) return RTM_OK;
     CK(cudaSetDevice(s.dev));
-    const size_t nbuf = (size_t)c->nx * c->ny * s.buf_planes();
+    const size_t nbuf = dplane(c) * s.buf_planes();
     for (int b = 0; b < 2; ++b) {
         if (cudaMalloc(&s.alt[b], nbuf * sizeof(float)) != cudaSuccess) {
             cudaGetLastError();
@@ -629,18 +637,19 @@ int tb_pass(rtm_ctx* c, Slab& s, int parity, cudaStream_t st) {
     RET(tb_alloc(c, s));
     CUtensorMap tm[6];
     const int np = (int)s.buf_planes();
-    RET(encode_3d(&tm[0], s.buf[parity], c->nx, c->ny, np, tv.TX + 16, tv.TY + 10));  // u^n box
-    RET(encode_3d(&tm[1], s.buf[parity ^ 1], c->nx, c->ny, np, tv.TX, tv.TY));        // u^{n-1}
-    RET(encode_3d(&tm[2], s.C, c->nx, c->ny, s.nzl, tv.TX, tv.TY));                   // C
-    RET(encode_3d(&tm[3], s.alt[parity ^ 1], c->nx, c->ny, np, tv.TX + 16, tv.TY + 10));  // u^{n+1} box
-    RET(encode_3d(&tm[4], s.buf[parity], c->nx, c->ny, np, tv.TX, tv.TY));            // u^n tile
-    RET(encode_3d(&tm[5], s.alt[parity ^ 1], c->nx, c->ny, np, tv.TX, tv.TY));        // u^{n+1} store
+    RET(encode_3d(&tm[0], s.buf[parity], c, np, tv.TX + 16, tv.TY + 10));  // u^n box
+    RET(encode_3d(&tm[1], s.buf[parity ^ 1], c, np, tv.TX, tv.TY));        // u^{n-1}
+    RET(encode_3d(&tm[2], s.C, c, s.nzl, tv.TX, tv.TY));                   // C
+    RET(encode_3d(&tm[3], s.alt[parity ^ 1], c, np, tv.TX + 16, tv.TY + 10));  // u^{n+1} box
+    RET(encode_3d(&tm[4], s.buf[parity], c, np, tv.TX, tv.TY));            // u^n tile
+    RET(encode_3d(&tm[5], s.alt[parity ^ 1], c, np, tv.TX, tv.TY));        // u^{n+1} store
     TB2SParams q;
     std::memset(&q, 0, sizeof q);
     q.nx = c->nx;
     q.ny = c->ny;
     q.nzl = s.nzl;
-    q.plane = (long long)c->nx * c->ny;
+    q.pitch = c->px;
+    q.plane = (long long)dplane(c);
     q.coef[0] = 3.0f * c->coeffs[0];
     for (int k = 1; k < 6; ++k) q.coef[k] = c->coeffs[k];
     q.outB = s.alt[parity];
@@ -736,8 +745,9 @@ int step_resident(rtm_ctx* c, int nsteps) {
     p.nx = c->nx;
     p.ny = c->ny;
     p.nzl = s.nzl;
+    p.pitch = c->px;
     p.nshots = s.nshots;
-    p.plane = (long long)c->nx * c->ny;
+    p.plane = (long long)dplane(c);
     p.coef[0] = 3.0f * c->coeffs[0];
     for (int k = 1; k < 6; ++k) p.coef[k] = c->coeffs[k];
     p.buf0 = s.buf[0];
@@ -804,7 +814,7 @@ int step_single(rtm_ctx* c, int nsteps) {
 
 int exchange_local(rtm_ctx* c, int parity_next) {
     const int G = (int)c->slabs.size();
-    const size_t plane = (size_t)c->nx * c->ny;
+    const size_t plane = dplane(c);
     const size_t bytes = 5 * plane * sizeof(float);
     for (int r = 0; r < G; ++r) {
         Slab& s = c->slabs[r];
@@ -829,7 +839,7 @@ int exchange_local(rtm_ctx* c, int parity_next) {
 
 int exchange_nccl(rtm_ctx* c, int parity_next) {
     Slab& s = c->slabs[0];
-    const size_t plane = (size_t)c->nx * c->ny;
+    const size_t plane = dplane(c);
     const size_t cnt = 5 * plane;
     CK(cudaStreamWaitEvent(s.s_comm, s.ev_bnd, 0));
     float* b = s.buf[parity_next];
@@ -854,7 +864,7 @@ int exchange_nccl(rtm_ctx* c, int parity_next) {
 // pushes into r's halo (RAW) and their reads of the halo planes r is about to overwrite (WAR).
 int step_slabs_fused(rtm_ctx* c, int nsteps) {
     const int G = (int)c->slabs.size();
-    const size_t plane = (size_t)c->nx * c->ny;
+    const size_t plane = dplane(c);
     for (int k = 0; k < nsteps; ++k) {
         const int parity = (int)(c->step & 1);
         for (int r = 0; r < G; ++r) {
@@ -995,7 +1005,7 @@ int setup_signal(rtm_ctx* c) {
 int step_slabs_signal(rtm_ctx* c, int nsteps) {
     static PFN_waitv64 waitv = driver_fn<PFN_waitv64>("cuStreamWaitValue64");
     if (!waitv) return fail(RTM_ECUDA, "cuStreamWaitValue64 unavailable from the driver");
-    const size_t plane = (size_t)c->nx * c->ny;
+    const size_t plane = dplane(c);
     const unsigned long long g = c->sig_gen << 40;
     for (int k = 0; k < nsteps; ++k) {
         const int parity = (int)(c->step & 1);
@@ -1078,10 +1088,22 @@ int sync_all(rtm_ctx* c) {
 }
 
 // Copy host slab arrays (x fastest) into/out of the interior planes of a device buffer.
-int h2d_planes(rtm_ctx* c, Slab& s, float* dst_base, const float* host, cudaStream_t st) {
-    const size_t plane = (size_t)c->nx * c->ny;
-    CK(cudaMemcpyAsync(dst_base, host, plane * s.nzl * sizeof(float), cudaMemcpyHostToDevice, st));
+// Copy nplanes planes between an unpadded array (nx per row) and a pitched device field.
+// to_dev: src unpadded -> dst pitched; otherwise src pitched -> dst unpadded.
+int copy_planes(const rtm_ctx* c, void* dst, const void* src, size_t nplanes, bool to_dev,
+                cudaMemcpyKind kind, cudaStream_t st) {
+    const size_t rows = (size_t)c->ny * nplanes;
+    if (c->px == c->nx)
+        CK(cudaMemcpyAsync(dst, src, rows * c->nx * sizeof(float), kind, st));
+    else
+        CK(cudaMemcpy2DAsync(dst, (to_dev ? c->px : c->nx) * sizeof(float), src,
+                             (to_dev ? c->nx : c->px) * sizeof(float), c->nx * sizeof(float), rows,
+                             kind, st));
     return RTM_OK;
+}
+
+int h2d_planes(rtm_ctx* c, Slab& s, float* dst_base, const float* host, cudaStream_t st) {
+    return copy_planes(c, dst_base, host, s.nzl, true, cudaMemcpyHostToDevice, st);
 }
 
 int async_vcheck(rtm_ctx* c);
@@ -1089,22 +1111,24 @@ int async_vcheck(rtm_ctx* c);
 int set_velocity_impl(rtm_ctx* c, const float* v, bool device_ptr) {
     RET(async_vcheck(c));  // verdict of earlier rtm_set_velocity_async calls (synchronising)
     c->vel_set = false;
-    const size_t plane = (size_t)c->nx * c->ny;
+    const size_t plane = hplane(c);  // offsets into the caller's unpadded array
     for (auto& s : c->slabs) {
         CK(cudaSetDevice(s.dev));
         cudaStream_t st = s.stream();
         const float* src;
-        if (device_ptr) {
+        if (device_ptr && c->px == c->nx) {
             src = v + (size_t)(s.z0 - c->slabs[0].z0) * plane;
         } else {
-            // stage v in C and convert in place
-            const float* h = v + (c->mode == 1 ? (size_t)s.z0 * plane : 0);
-            RET(h2d_planes(c, s, s.C, h, st));
+            // stage v in C (pitched) and convert in place
+            const float* h = v + (device_ptr ? (size_t)(s.z0 - c->slabs[0].z0) * plane
+                                             : (c->mode == 1 ? (size_t)s.z0 * plane : 0));
+            RET(copy_planes(c, s.C, h, s.nzl, true,
+                            device_ptr ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
             src = s.C;
         }
         CK(cudaMemsetAsync(s.d_stats, 0, 2 * sizeof(unsigned int), st));
-        CK(launch_velocity(src, s.C, (long long)plane * s.nzl, (double)c->dt, (double)c->dx,
-                           s.d_stats, st));
+        CK(launch_velocity(src, s.C, (long long)(dplane(c) * s.nzl), c->nx, c->px, (double)c->dt,
+                           (double)c->dx, s.d_stats, st));
     }
     float vmax = 0.0f;
     unsigned long long bad = 0;
@@ -1128,17 +1152,17 @@ int set_velocity_impl(rtm_ctx* c, const float* v, bool device_ptr) {
 }
 
 int reset_impl(rtm_ctx* c, const float* u, const float* up) {
-    const size_t plane = (size_t)c->nx * c->ny;
+    const size_t plane = hplane(c), dpl = dplane(c);
     for (auto& s : c->slabs) {
         CK(cudaSetDevice(s.dev));
         cudaStream_t st = s.stream();
         CK(cudaStreamSynchronize(s.s_comm));
-        const size_t nbuf = plane * s.buf_planes();
+        const size_t nbuf = dpl * s.buf_planes();
         for (int b = 0; b < 2; ++b) CK(cudaMemsetAsync(s.buf[b], 0, nbuf * sizeof(float), st));
         const size_t off = c->mode == 1 ? (size_t)s.z0 * plane : 0;
         for (int k = 0; k < s.nshots; ++k) {  // host arrays: (nshots, nz, ny, nx)
             const size_t hoff = off + (size_t)k * plane * s.nzl;
-            const size_t doff = ((size_t)k * (s.nzl + 10) + 5) * plane;
+            const size_t doff = ((size_t)k * (s.nzl + 10) + 5) * dpl;
             if (u) RET(h2d_planes(c, s, s.buf[0] + doff, u + hoff, st));
             if (up) RET(h2d_planes(c, s, s.buf[1] + doff, up + hoff, st));
         }
@@ -1162,15 +1186,15 @@ int reset_impl(rtm_ctx* c, const float* u, const float* up) {
 }
 
 int read_impl(rtm_ctx* c, float* out, int which /*0 = u^n, 1 = u^{n-1}*/) {
-    const size_t plane = (size_t)c->nx * c->ny;
+    const size_t plane = hplane(c), dpl = dplane(c);
     const int par = (int)((c->step + which) & 1);
     for (auto& s : c->slabs) {
         CK(cudaSetDevice(s.dev));
         const size_t off = c->mode == 1 ? (size_t)s.z0 * plane : 0;
         for (int k = 0; k < s.nshots; ++k)
-            CK(cudaMemcpyAsync(out + off + (size_t)k * plane * s.nzl,
-                               s.buf[par] + ((size_t)k * (s.nzl + 10) + 5) * plane,
-                               plane * s.nzl * sizeof(float), cudaMemcpyDeviceToHost, s.stream()));
+            RET(copy_planes(c, out + off + (size_t)k * plane * s.nzl,
+                            s.buf[par] + ((size_t)k * (s.nzl + 10) + 5) * dpl, s.nzl, false,
+                            cudaMemcpyDeviceToHost, s.stream()));
     }
     return sync_all(c);
 }
@@ -1186,10 +1210,11 @@ int async_setup(rtm_ctx* c, bool need_stage, bool need_snap) {
         for (cudaEvent_t* e : {&c->ev_h2d, &c->ev_conv, &c->ev_snap, &c->ev_d2h})
             CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
-    const size_t n = (size_t)c->nx * c->ny * s.nzl;
-    if (need_stage && !c->v_stage && cudaMalloc(&c->v_stage, n * sizeof(float)) != cudaSuccess) {
+    const size_t n = hplane(c) * s.nzl;  // the snapshot is unpadded (host layout)
+    const size_t nst = dplane(c) * s.nzl;  // the velocity staging is pitched (device layout)
+    if (need_stage && !c->v_stage && cudaMalloc(&c->v_stage, nst * sizeof(float)) != cudaSuccess) {
         cudaGetLastError();
-        return fail(RTM_ENOMEM, "velocity staging buffer (%zu bytes)", n * 4);
+        return fail(RTM_ENOMEM, "velocity staging buffer (%zu bytes)", nst * 4);
     }
     if (need_snap && !c->snap && cudaMalloc(&c->snap, n * s.nshots * sizeof(float)) != cudaSuccess) {
         cudaGetLastError();
@@ -1547,11 +1572,11 @@ int rtm_read_field_device(rtm_ctx* c, float* d_out) {
     DeviceGuard g;
     Slab& s = c->slabs[0];
     CK(cudaSetDevice(s.dev));
-    const size_t plane = (size_t)c->nx * c->ny;
+    const size_t plane = hplane(c), dpl = dplane(c);
     for (int k = 0; k < s.nshots; ++k)
-        CK(cudaMemcpyAsync(d_out + (size_t)k * plane * s.nzl,
-                           s.buf[c->step & 1] + ((size_t)k * (s.nzl + 10) + 5) * plane,
-                           plane * s.nzl * sizeof(float), cudaMemcpyDeviceToDevice, s.stream()));
+        RET(copy_planes(c, d_out + (size_t)k * plane * s.nzl,
+                        s.buf[c->step & 1] + ((size_t)k * (s.nzl + 10) + 5) * dpl, s.nzl, false,
+                        cudaMemcpyDeviceToDevice, s.stream()));
     return RTM_OK;
 }
 
@@ -1567,7 +1592,7 @@ int rtm_reset(rtm_ctx* c) {
     if (c->mode == 0) {  // enqueue only (the bench times reset inside a step)
         Slab& s = c->slabs[0];
         CK(cudaSetDevice(s.dev));
-        const size_t nbuf = (size_t)c->nx * c->ny * s.buf_planes();
+        const size_t nbuf = dplane(c) * s.buf_planes();
         for (int b = 0; b < 2; ++b) CK(cudaMemsetAsync(s.buf[b], 0, nbuf * sizeof(float), s.stream()));
         CK(cudaMemsetAsync(s.d_step, 0, 2 * sizeof(int), s.stream()));
         c->step = 0;
@@ -1620,7 +1645,7 @@ int rtm_set_step_count(rtm_ctx* c, long long n) {
 int rtm_field_stats(rtm_ctx* c, double* max_abs, long long* nonfinite) {
     if (!c) return fail(RTM_EINVAL, "ctx is NULL");
     DeviceGuard g;
-    const long long plane = (long long)c->nx * c->ny;
+    const long long plane = (long long)dplane(c);  // padding columns are zero: no effect on stats
     double m = 0;
     long long bad = 0;
     for (auto& s : c->slabs) {
@@ -1644,8 +1669,6 @@ int rtm_set_tile(rtm_ctx* c, int tile_id) {
     if (!c) return fail(RTM_EINVAL, "ctx is NULL");
     if (tile_id < -1 || tile_id >= num_variants())
         return fail(RTM_EINVAL, "unknown tile id %d (valid: -1 .. %d)", tile_id, num_variants() - 1);
-    if (tile_id > 0 && c->nx % 4 != 0)
-        return fail(RTM_EINVAL, "tiled variants need nx %% 4 == 0 (nx=%d)", c->nx);
     c->tile = tile_id;
     invalidate_graphs(c);
     return RTM_OK;
@@ -1799,16 +1822,11 @@ int rtm_autotune(rtm_ctx* c, int nI, const int* tiles, const int* zchunks, int n
         for (int k = 0; k < ncand; ++k) {
             if (tiles[k] < 0 || tiles[k] >= num_variants())
                 return fail(RTM_EINVAL, "candidate %d: unknown tile %d", k, tiles[k]);
-            if (tiles[k] > 0 && c->nx % 4 != 0)
-                return fail(RTM_EINVAL, "candidate %d: tiled variants need nx %% 4 == 0", k);
             const int z = zchunks ? zchunks[k] : 0;
             if (z < 0) return fail(RTM_EINVAL, "candidate %d: z-chunk %d < 0", k, z);
             ct.push_back(tiles[k]);
             cz.push_back(z);
         }
-    } else if (c->nx % 4 != 0) {  // only the naive kernel handles nx % 4 != 0
-        ct.push_back(0);
-        cz.push_back(0);
     } else {
         for (int t = 1; t < num_variants(); ++t) {
             ct.push_back(t);
@@ -1834,7 +1852,7 @@ int rtm_autotune(rtm_ctx* c, int nI, const int* tiles, const int* zchunks, int n
     for (size_t k = 0; k < c->slabs.size() && rc == RTM_OK; ++k) {
         Slab& s = c->slabs[k];
         cudaSetDevice(s.dev);
-        const size_t bytes = (size_t)c->nx * c->ny * s.buf_planes() * sizeof(float);
+        const size_t bytes = dplane(c) * s.buf_planes() * sizeof(float);
         for (int b = 0; b < 2 && rc == RTM_OK; ++b) {
             if (cudaMalloc(&snap[2 * k + b], bytes) != cudaSuccess) {
                 cudaGetLastError();
@@ -1878,7 +1896,7 @@ int rtm_autotune(rtm_ctx* c, int nI, const int* tiles, const int* zchunks, int n
     for (size_t k = 0; k < c->slabs.size(); ++k) {
         Slab& s = c->slabs[k];
         cudaSetDevice(s.dev);
-        const size_t bytes = (size_t)c->nx * c->ny * s.buf_planes() * sizeof(float);
+        const size_t bytes = dplane(c) * s.buf_planes() * sizeof(float);
         for (int b = 0; b < 2; ++b)
             if (snap[2 * k + b])
                 cudaMemcpyAsync(s.buf[b], snap[2 * k + b], bytes, cudaMemcpyDeviceToDevice, s.stream());
@@ -1944,14 +1962,15 @@ int rtm_set_velocity_async(rtm_ctx* c, const float* v) {
     DeviceGuard g;
     RET(async_setup(c, true, false));
     Slab& s = c->slabs[0];
-    const size_t n = (size_t)c->nx * c->ny * s.nzl;
+    const size_t n = dplane(c) * s.nzl;
     cudaStream_t st = s.stream();
     if (!c->vcheck_pending) CK(cudaMemsetAsync(s.d_stats, 0, 2 * sizeof(unsigned int), st));
     CK(cudaStreamWaitEvent(c->s_h2d, c->ev_conv, 0));  // the previous conversion read v_stage
-    CK(cudaMemcpyAsync(c->v_stage, v, n * sizeof(float), cudaMemcpyHostToDevice, c->s_h2d));
+    RET(copy_planes(c, c->v_stage, v, s.nzl, true, cudaMemcpyHostToDevice, c->s_h2d));
     CK(cudaEventRecord(c->ev_h2d, c->s_h2d));
     CK(cudaStreamWaitEvent(st, c->ev_h2d, 0));  // C changes after the steps already enqueued
-    CK(launch_velocity(c->v_stage, s.C, (long long)n, (double)c->dt, (double)c->dx, s.d_stats, st));
+    CK(launch_velocity(c->v_stage, s.C, (long long)n, c->nx, c->px, (double)c->dt, (double)c->dx,
+                       s.d_stats, st));
     CK(cudaEventRecord(c->ev_conv, st));
     c->vcheck_pending = true;
     c->vel_set = true;  // provisional: rtm_sync returns the verdict
@@ -1977,12 +1996,12 @@ int rtm_read_field_async(rtm_ctx* c, float* out) {
     DeviceGuard g;
     RET(async_setup(c, false, true));
     Slab& s = c->slabs[0];
-    const size_t plane = (size_t)c->nx * c->ny, n = plane * s.nzl;
+    const size_t n = hplane(c) * s.nzl, dpl = dplane(c);
     cudaStream_t st = s.stream();
     CK(cudaStreamWaitEvent(st, c->ev_d2h, 0));  // the previous D2H has read the snapshot
-    for (int k = 0; k < s.nshots; ++k)
-        CK(cudaMemcpyAsync(c->snap + (size_t)k * n, s.buf[c->step & 1] + ((size_t)k * (s.nzl + 10) + 5) * plane,
-                           n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    for (int k = 0; k < s.nshots; ++k)  // unpadded snapshot of the interior
+        RET(copy_planes(c, c->snap + (size_t)k * n, s.buf[c->step & 1] + ((size_t)k * (s.nzl + 10) + 5) * dpl,
+                        s.nzl, false, cudaMemcpyDeviceToDevice, st));
     CK(cudaEventRecord(c->ev_snap, st));
     CK(cudaStreamWaitEvent(c->s_copy, c->ev_snap, 0));
     CK(cudaMemcpyAsync(out, c->snap, n * s.nshots * sizeof(float), cudaMemcpyDeviceToHost, c->s_copy));

@@ -21,7 +21,9 @@ struct DevSource {       // a source owned by this slab, LOCAL coordinates
 // Everything a stencil launch needs.  Passed by value (__grid_constant__).
 struct StencilParams {
     int nx, ny, nzl;           // interior extents of this slab
-    long long plane;           // nx*ny
+    int pitch;                 // row stride in floats: nx rounded up to a multiple of 4; the
+                               // padding columns [nx, pitch) are zero at all times
+    long long plane;           // pitch*ny
     int nshots;                // independent wavefields sharing C (batched shots); shot k's
                                // planes start at buffer plane k*(nzl+10)
     float coef[6];             // coef[0] = 3*c0 (fp32, host-folded), coef[1..5] = c1..c5
@@ -95,6 +97,7 @@ cudaError_t launch_naive(const StencilParams& p, cudaStream_t s);
 // launcher) between steps; buffers alternate starting from buf[parity0] = u^n.
 struct ResParams {
     int nx, ny, nzl, nshots;
+    int pitch;
     long long plane;
     float coef[6];
     float* buf0;
@@ -116,6 +119,7 @@ cudaError_t resident_occupancy(int threads, int* per_sm);
 // reports progress (flagsB) that throttles stage A.
 struct TB2SParams {
     int nx, ny, nzl;
+    int pitch;
     long long plane;
     float coef[6];
     float* outB;                        // u^{n+2} (stage-B STG stores, band rows only)
@@ -146,8 +150,10 @@ cudaError_t tb2s_variant_fn(int id, const void** fn, int* threads, size_t* smem)
 // non-finite values, over the owned planes of every shot in a slab buffer.
 cudaError_t launch_field_stats(const float* buf, long long plane, int nzl, int nshots,
                                unsigned int* stats, cudaStream_t s);
-cudaError_t launch_velocity(const float* v, float* C, long long n, double dt, double dx,
-                            unsigned int* stats, cudaStream_t s);
+// v and C are pitched (row stride pitch floats, n = pitch * rows); padding columns x >= nx get
+// C = 0 and do not enter the statistics.
+cudaError_t launch_velocity(const float* v, float* C, long long n, int nx, int pitch, double dt,
+                            double dx, unsigned int* stats, cudaStream_t s);
 // st.release.sys of v into *lo and *hi (either may be null) after a system fence
 cudaError_t launch_signal(unsigned long long* lo, unsigned long long* hi, unsigned long long v,
                           cudaStream_t s);

@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(TX * TY / 4, MINB)
         p.d_step[p.parity ^ 1] = p.d_step[p.parity] + 1;
 
     const int own = (5 + ty) * S::RS + 8 + 4 * tx;
-    const long long col = (long long)y * p.nx + x;
+    const long long col = (long long)y * p.pitch + x;
 
     // ---- prologue: queue <- planes zs-5 .. zs+4
     float4 q[11];
@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(TX * TY / 4, MINB)
         }
         if (smask) add_sources(p, smask, x, z, out);
         if (active) {
+            zero_pad(out, x, p.nx);
             const float4 o4 = make_float4(out[0], out[1], out[2], out[3]);
             st_stream4(p.next + (soff + z + 5) * p.plane + col, o4);
             push_halo4(p, z, col, o4);
@@ -217,15 +218,16 @@ __global__ void __launch_bounds__(256) k_naive(const __grid_constant__ StencilPa
             z = p.r_begin[1] + static_cast<int>(tt / p.plane);
         }
         const long long inplane = tt % p.plane;
-        const int y = static_cast<int>(inplane / p.nx);
-        const int x = static_cast<int>(inplane - (long long)y * p.nx);
+        const int y = static_cast<int>(inplane / p.pitch);
+        const int x = static_cast<int>(inplane - (long long)y * p.pitch);
+        if (x >= p.nx) continue;  // padding column: stays zero
         const long long pb = ((long long)shot * (p.nzl + 10) + z + 5) * p.plane + inplane;  // buffer index
         float zl[11], yl[11], xl[11];
 #pragma unroll
         for (int o = -5; o <= 5; ++o) {
             zl[o + 5] = p.u[pb + o * p.plane];  // z-halo planes are explicit
             const int yy = y + o, xx = x + o;
-            yl[o + 5] = (yy >= 0 && yy < p.ny) ? p.u[pb + (long long)o * p.nx] : 0.0f;
+            yl[o + 5] = (yy >= 0 && yy < p.ny) ? p.u[pb + (long long)o * p.pitch] : 0.0f;
             xl[o + 5] = (xx >= 0 && xx < p.nx) ? p.u[pb + o] : 0.0f;
         }
         float out = rtm_point(zl, yl, xl, p.next[pb], p.C[(long long)z * p.plane + inplane], c);
@@ -254,9 +256,11 @@ __device__ __forceinline__ float c_of_v(float vi, double dt, double dx, float& v
 }
 
 // vec4: n % 4 == 0 and 16-byte aligned pointers -> 128-bit loads/stores, 4 independent
-// fp64 chains per thread (the scalar form was latency-bound at ~2 TB/s).
-__global__ void __launch_bounds__(256) k_velocity(const float* v, float* C, long long n, double dt,
-                                                  double dx, unsigned int* stats, int vec4) {
+// fp64 chains per thread (the scalar form was latency-bound at ~2 TB/s).  Padding columns
+// (x = i mod pitch >= nx) get C = 0 and stay out of the statistics.
+__global__ void __launch_bounds__(256) k_velocity(const float* v, float* C, long long n, int nx,
+                                                  int pitch, double dt, double dx,
+                                                  unsigned int* stats, int vec4) {
     float vmax = 0.0f;
     unsigned int bad = 0;
     const long long stride = (long long)gridDim.x * blockDim.x;
@@ -267,14 +271,23 @@ __global__ void __launch_bounds__(256) k_velocity(const float* v, float* C, long
         for (long long i = t0; i < n / 4; i += stride) {
             const float4 a = __ldcs(v4 + i);
             float4 r;
-            r.x = c_of_v(a.x, dt, dx, vmax, bad);
-            r.y = c_of_v(a.y, dt, dx, vmax, bad);
-            r.z = c_of_v(a.z, dt, dx, vmax, bad);
-            r.w = c_of_v(a.w, dt, dx, vmax, bad);
+            const int x = static_cast<int>((4 * i) % pitch);
+            if (x + 4 <= nx) {
+                r.x = c_of_v(a.x, dt, dx, vmax, bad);
+                r.y = c_of_v(a.y, dt, dx, vmax, bad);
+                r.z = c_of_v(a.z, dt, dx, vmax, bad);
+                r.w = c_of_v(a.w, dt, dx, vmax, bad);
+            } else {  // the group holding the last columns and the padding
+                float o[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) o[k] = x + k < nx ? c_of_v(o[k], dt, dx, vmax, bad) : 0.0f;
+                r = make_float4(o[0], o[1], o[2], o[3]);
+            }
             c4[i] = r;
         }
     } else {
-        for (long long i = t0; i < n; i += stride) C[i] = c_of_v(v[i], dt, dx, vmax, bad);
+        for (long long i = t0; i < n; i += stride)
+            C[i] = (int)(i % pitch) < nx ? c_of_v(v[i], dt, dx, vmax, bad) : 0.0f;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -462,7 +475,7 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
                     smask |= (1ull << s);
             }
         }
-        const long long col = (long long)y * p.nx + x;
+        const long long col = (long long)y * p.pitch + x;
         float* outp = p.next + (g.soff + g.zs + 5) * p.plane + col;  // also u_prev (D == 0)
         const float* cp = p.C + (long long)g.zs * p.plane + col;
 
@@ -565,6 +578,7 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
             }
             if (smask) add_sources(p, smask, x, g.zs + it, out);
             if (active) {
+                zero_pad(out, x, p.nx);
                 const float4 o4 = make_float4(out[0], out[1], out[2], out[3]);
                 st_mode4(outp, o4, plain);
                 if (p.push_lo || p.push_hi) push_halo4(p, g.zs + it, col, o4);
@@ -810,14 +824,14 @@ cudaError_t launch_signal(unsigned long long* lo, unsigned long long* hi, unsign
     return cudaGetLastError();
 }
 
-cudaError_t launch_velocity(const float* v, float* C, long long n, double dt, double dx,
-                            unsigned int* stats, cudaStream_t s) {
+cudaError_t launch_velocity(const float* v, float* C, long long n, int nx, int pitch, double dt,
+                            double dx, unsigned int* stats, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     const int vec4 = (n % 4 == 0) && (reinterpret_cast<uintptr_t>(v) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(C) % 16 == 0);
     long long blocks = ((vec4 ? n / 4 : n) + 255) / 256;
     if (blocks > 148LL * 8) blocks = 148LL * 8;
-    k_velocity<<<static_cast<unsigned>(blocks), 256, 0, s>>>(v, C, n, dt, dx, stats, vec4);
+    k_velocity<<<static_cast<unsigned>(blocks), 256, 0, s>>>(v, C, n, nx, pitch, dt, dx, stats, vec4);
     return cudaGetLastError();
 }
 

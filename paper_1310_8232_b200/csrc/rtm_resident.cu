@@ -51,7 +51,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
 template <int NT>
 __global__ void __launch_bounds__(NT) k_resident(const __grid_constant__ ResParams p) {
     const float c[6] = {p.coef[0], p.coef[1], p.coef[2], p.coef[3], p.coef[4], p.coef[5]};
-    const int nxq = p.nx >> 2;
+    const int nxq = p.pitch >> 2;  // 4-point groups per pitched row
     const long long per_shot = (long long)p.nzl * p.ny * nxq;
     const long long total = per_shot * p.nshots;
     const int n0 = p.d_step[p.parity0];
@@ -69,7 +69,8 @@ __global__ void __launch_bounds__(NT) k_resident(const __grid_constant__ ResPara
             r -= (long long)z * p.ny * nxq;
             const int y = static_cast<int>(r / nxq);
             const int x = 4 * static_cast<int>(r - (long long)y * nxq);
-            const long long inpl = (long long)y * p.nx + x;
+            if (x >= p.nx) continue;  // a group of padding columns: stays zero
+            const long long inpl = (long long)y * p.pitch + x;
             const long long base = ((long long)shot * (p.nzl + 10) + z + 5) * p.plane + inpl;
             float4 q[11];
 #pragma unroll
@@ -78,8 +79,8 @@ __global__ void __launch_bounds__(NT) k_resident(const __grid_constant__ ResPara
             const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
             for (int m = 1; m <= 5; ++m) {
-                yv[5 - m] = y - m >= 0 ? ldcg4(u + base - (long long)m * p.nx) : zero;
-                yv[5 + m] = y + m < p.ny ? ldcg4(u + base + (long long)m * p.nx) : zero;
+                yv[5 - m] = y - m >= 0 ? ldcg4(u + base - (long long)m * p.pitch) : zero;
+                yv[5 + m] = y + m < p.ny ? ldcg4(u + base + (long long)m * p.pitch) : zero;
             }
             yv[5] = q[5];
             float xs[14];
@@ -107,6 +108,7 @@ __global__ void __launch_bounds__(NT) k_resident(const __grid_constant__ ResPara
                         if (kk == i) out[kk] = __fadd_rn(out[kk], w);
                 }
             }
+            zero_pad(out, x, p.nx);
             __stcg(reinterpret_cast<float4*>(nxt + base), make_float4(out[0], out[1], out[2], out[3]));
         }
         grid_barrier(p.bar, gen);

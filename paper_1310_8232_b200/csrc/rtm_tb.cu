@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(TB2SShape<TX, TY, K, D, 4>::NT, 2)
             if (src.shot == 0 && src.y == y && src.x >= x && src.x < x + 4) smask |= (1ull << s);
         }
     }
-    const long long col = (long long)y * p.nx + x;
+    const long long col = (long long)y * p.pitch + x;
     float* outB = p.outB + 5 * p.plane + col;
     const uint32_t fu = smem_u32(full_u), eu = smem_u32(empty_u);
     const uint32_t fc = smem_u32(full_c), ec = smem_u32(empty_c);
@@ -376,6 +376,7 @@ __global__ void __launch_bounds__(TB2SShape<TX, TY, K, D, 4>::NT, 2)
             mbar_arrive_u32(ec + 8 * sq);
         }
         if (smask) add_sources_2s(p, smask, x, it, nS, out);
+        zero_pad(out, x, p.nx);  // (A: the TMA store clips at nx anyway)
         const float4 o4 = make_float4(out[0], out[1], out[2], out[3]);
         if (isA) {
             const int slot = it % S_;
