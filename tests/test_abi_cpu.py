@@ -120,6 +120,11 @@ def test_sass_has_tma_and_no_legacy_tensor_ops():
     assert "UTMALDG" in sass
     assert "SYNCS" in sass  # mbarrier operations
     assert "HMMA" not in sass
+    # Blackwell-specific instructions the design relies on: packed FP32x2
+    # arithmetic of the point update, TMA tensor stores of the two-step publication, and the
+    # programmatic-dependent-launch wait / trigger of k_stream (griddepcontrol)
+    for m in ("FFMA2", "FADD2", "UTMASTG", "ACQBULK", "PREEXIT"):
+        assert m in sass, m
 
 
 def test_select_mwmb_is_eq2_minmax(P):
