@@ -1034,3 +1034,33 @@ def test_ragged_nx_slabs_async_dist_and_device_velocity(P):
         P.rtm_read_field_async(sim.h, out)
         P.rtm_sync(sim.h)
         assert np.array_equal(out, ref)
+
+
+def test_bench_line_contract_and_consistency(P):
+    """bench.py (C1, 3 steps) prints one JSON line with the driver's keys, and its roofline
+    fields are self-consistent: achieved = alg bytes per launch / average launch time,
+    frac = achieved / peak; e2e counts its H2D / D2H bytes; launches are counted."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--config", "1", "--steps", "3",
+                        "--warmup", "3", "--no-cpu"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "roofline",
+              "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["value"] > 0 and d["gpu_launches"] > 0
+    rf = d["roofline"]
+    achieved = rf["alg_bytes_per_launch"] / (rf["avg_launch_ms"] / 1e3) / 1e9
+    assert abs(achieved - rf["achieved"]) <= 0.01 * rf["achieved"] + 1.0
+    assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) <= 1e-3
+    nbytes = 64 ** 3 * 4
+    assert d["e2e"]["h2d_bytes_per_step"] == nbytes and d["e2e"]["d2h_bytes_per_step"] == nbytes
+    assert d["e2e"]["value"] > 0 and d["e2e"]["matches_device_result"] is True
+    assert d["config"]["workload"] == "C1" and d["clocks"]["sm_max_mhz"]
