@@ -1,0 +1,80 @@
+"""Randomised parity fuzz (GPU): random ragged shapes, velocities, initial conditions, sources
+and step counts; every kernel variant must equal the naive kernel bitwise and the fp32 oracle
+within the one-step tolerance scaled by the step count; slab decompositions (halo modes 0-2)
+must equal the single-slab result bitwise.  Usage: python tools/fuzz_parity.py [cases] [seed]"""
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+import oracle  # noqa: E402  (test infrastructure: the fuzz is a test)
+import paper_1310_8232_b200 as P  # noqa: E402
+import rtm_inputs as ri  # noqa: E402
+
+C32 = ri.COEFFS_F32
+
+
+def run(v, steps, u0, up0, src, tile=None, devices=None, halo=0):
+    nz, ny, nx = v.shape
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, devices=devices) as sim:
+        if halo:
+            P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, halo)
+        if tile is not None:
+            sim.set_tile(tile)
+        sim.set_velocity(v)
+        for s in src:
+            sim.inject_source(*s)
+        sim.set_fields(u0, up0)
+        sim.step(steps)
+        return sim.read_field()
+
+
+def main():
+    cases = int(sys.argv[1]) if len(sys.argv) > 1 else 60
+    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 2024)
+    scale = float(sys.argv[3]) if len(sys.argv) > 3 else 1.0  # size multiplier
+    ntiles = P.rtm_num_tiles()
+    fails = 0
+    t0 = time.time()
+    for c in range(cases):
+        nz = int(rng.integers(1, int(41 * scale) + 1))
+        ny = int(rng.integers(1, int(71 * scale) + 1))
+        nx = int(rng.integers(1, int(141 * scale) + 1))
+        steps = int(rng.integers(1, int(10 * scale) + 1))
+        v = rng.uniform(1500, 4300, (nz, ny, nx)).astype(np.float32)
+        u0, up0 = ri.random_fields(v.shape, seed=int(rng.integers(1 << 30)))
+        src = []
+        for _ in range(int(rng.integers(0, 5))):
+            w = ri.source_samples(float(rng.uniform(1500, 4300)), 1e-3, 15.0, steps)
+            src.append((int(rng.integers(nx)), int(rng.integers(ny)), int(rng.integers(nz)), w))
+        ref = oracle.run(v, 10.0, 1e-3, C32, steps, u0=u0, up0=up0, sources=src)
+        base = run(v, steps, u0, up0, src, tile=0)
+        m = float(np.abs(ref).max()) or 1.0
+        err = float(np.abs(base.astype(np.float64) - ref).max()) / m
+        bad = []
+        if err > 1e-5 * max(steps, 1) * 2:
+            bad.append(f"naive vs oracle {err:.2e}")
+        for t in range(1, ntiles):
+            out = run(v, steps, u0, up0, src, tile=t)
+            if not np.array_equal(out, base):
+                d = out != base
+                bad.append(f"{P.rtm_tile_name(t)}: {int(d.sum())} pts differ")
+        for G in (2, 3):
+            if nz >= 10 * G:
+                for halo in (0, 1, 2):
+                    out = run(v, steps, u0, up0, src, devices=[0] * G, halo=halo)
+                    if not np.array_equal(out, base):
+                        bad.append(f"slabs G={G} halo={halo}")
+        status = "OK" if not bad else "FAIL " + "; ".join(bad[:4])
+        fails += bool(bad)
+        print(f"case {c:3d} shape=({nz},{ny},{nx}) steps={steps} src={len(src)} oracle_err={err:.1e} {status}",
+              flush=True)
+    print(f"{cases} cases, {fails} failing, {time.time() - t0:.0f} s", flush=True)
+    return 1 if fails else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
