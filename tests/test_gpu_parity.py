@@ -1064,3 +1064,22 @@ def test_bench_line_contract_and_consistency(P):
     assert d["e2e"]["h2d_bytes_per_step"] == nbytes and d["e2e"]["d2h_bytes_per_step"] == nbytes
     assert d["e2e"]["value"] > 0 and d["e2e"]["matches_device_result"] is True
     assert d["config"]["workload"] == "C1" and d["clocks"]["sm_max_mhz"]
+
+
+def test_randomized_parity_fuzz_slice(P):
+    """40 cases of tools/fuzz_parity.py (random ragged shapes, velocities, ICs, sources, step
+    counts): every variant bitwise equal to the naive kernel, slab modes bitwise equal to the
+    single slab, the naive kernel within tolerance of the oracle."""
+    import importlib.util
+    import sys
+    from pathlib import Path
+    path = Path(__file__).resolve().parent.parent / "tools" / "fuzz_parity.py"
+    spec = importlib.util.spec_from_file_location("fuzz_parity", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    argv = sys.argv
+    try:
+        sys.argv = ["fuzz_parity.py", "40", "99", "1.0"]
+        assert mod.main() == 0
+    finally:
+        sys.argv = argv
