@@ -17,17 +17,41 @@ import rtm_inputs as ri  # noqa: E402
 C32 = ri.COEFFS_F32
 
 
-def run(v, steps, u0, up0, src, tile=None, devices=None, halo=0):
+def run(v, steps, u0, up0, src, tile=None, devices=None, halo=0, tb_ctas=0, asyn=False):
     nz, ny, nx = v.shape
     with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, devices=devices) as sim:
         if halo:
             P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, halo)
         if tile is not None:
             sim.set_tile(tile)
-        sim.set_velocity(v)
+        if tb_ctas:
+            P.rtm_set_option(sim.h, P.RTM_OPT_TB_CTAS, tb_ctas)
+        if asyn:
+            P.rtm_set_velocity_async(sim.h, v)
+        else:
+            sim.set_velocity(v)
         for s in src:
             sim.inject_source(*s)
         sim.set_fields(u0, up0)
+        if asyn:
+            out = np.empty(v.shape, np.float32)
+            P.rtm_step_async(sim.h, steps)
+            P.rtm_read_field_async(sim.h, out)
+            P.rtm_sync(sim.h)
+            return out
+        sim.step(steps)
+        return sim.read_field()
+
+
+def run_shots(v, steps, u0, up0, src, tile):
+    """Two shots: shot 0 = (u0, up0, src), shot 1 = (up0, u0, no source)."""
+    nz, ny, nx = v.shape
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, shots=2) as sim:
+        sim.set_tile(tile)
+        sim.set_velocity(v)
+        for (x, y, z, w) in src:
+            P.rtm_inject_source_shot(sim.h, 0, x, y, z, w)
+        sim.set_fields(np.stack([u0, up0]), np.stack([up0, u0]))
         sim.step(steps)
         return sim.read_field()
 
@@ -62,6 +86,20 @@ def main():
             if not np.array_equal(out, base):
                 d = out != base
                 bad.append(f"{P.rtm_tile_name(t)}: {int(d.sum())} pts differ")
+        tbs = [t for t in range(ntiles) if (P.rtm_tile_name(t) or "").startswith("tb2")]
+        for t in tbs[:1]:  # multi-band two-step plans
+            ctas = int(rng.integers(1, 13))
+            out = run(v, steps, u0, up0, src, tile=t, tb_ctas=ctas)
+            if not np.array_equal(out, base):
+                bad.append(f"{P.rtm_tile_name(t)} tb_ctas={ctas}")
+        out = run(v, steps, u0, up0, src, asyn=True)
+        if not np.array_equal(out, base):
+            bad.append("async pipeline")
+        t_sh = int(rng.integers(0, ntiles))
+        sh = run_shots(v, steps, u0, up0, src, t_sh)
+        other = run(v, steps, up0, u0, [], tile=0)
+        if not (np.array_equal(sh[0], base) and np.array_equal(sh[1], other)):
+            bad.append(f"2 shots ({P.rtm_tile_name(t_sh)})")
         for G in (2, 3):
             if nz >= 10 * G:
                 for halo in (0, 1, 2):
