@@ -147,26 +147,48 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ reference arm
+def bench_config(cfg, world, shots, halo, nsteps):
+    """The `config` object of the JSON line — identical in both arms (workload only; the
+    kernel variant the autotuner picks is reported outside it)."""
+    nzl = cfg.nz // world if world > 1 else cfg.nz
+    wl = f"C{cfg.k}" if shots == 1 else f"C{cfg.k}x{shots}shots"
+    return {"workload": wl, "grid": [cfg.nx, cfg.ny, cfg.nz], "time_steps": nsteps,
+            "sources": len(cfg.sources_xyz), "shots": shots,
+            "parallelism": f"z-slab x{world}",
+            "halo": ({0: "NCCL send/recv", 2: "fused IPC push + flags",
+                      3: "IPC copy-engine pull"}.get(halo)) if world > 1 else None,
+            "l2": "inputs larger than L2 (3 fields > 126 MB)"
+            if cfg.nx * cfg.ny * nzl * shots * 4 > 126e6 else "L2-resident (no flush)"}
+
+
+def oracle_sample(cfg, v_full, planes_per_mib):
+    """The bounded CPU sample of the workload both CPU legs time: the first planes of the
+    velocity model (about planes_per_mib planes of 1024x1024, at least 10)."""
+    planes = max(10, min(cfg.nz, int(planes_per_mib * (1024 * 1024) / (cfg.nx * cfg.ny))))
+    return np.ascontiguousarray(v_full[:planes]), planes
+
+
 def run_reference(args):
-    """--impl reference: the CPU oracle as it stands, on a bounded sample of the workload."""
+    """--impl reference: the CPU oracle as it stands, on a bounded sample of the workload.
+    Timed like cpu_baseline: the oracle's own steady_clock around its step loop (allocation,
+    C(p) set-up and copies excluded), on the same sample (first 64 z-planes of the config)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     import oracle
     import rtm_inputs as ri
     cfg = ri.make_config(args.config, G=args.gpus if args.config == 5 else 1)
+    nsteps_cfg = args.nsteps or cfg.steps
     v_full = cfg.velocity()
-    planes = max(10, min(cfg.nz, int(16 * (1024 * 1024) / (cfg.nx * cfg.ny))))
-    v = np.ascontiguousarray(v_full[:planes])
-    nsteps = 2
+    v, planes = oracle_sample(cfg, v_full, 64)
+    nsteps = 8  # time steps per bench step (~1 s of host work per bench step at C4)
     srcs = [(x, y, z, w[:nsteps]) for (x, y, z, w) in cfg.sources(v_full) if z < planes]
     cores = len(os.sched_getaffinity(0))
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
 
     def one():
-        t = time.perf_counter()
         oracle.run(v, cfg.dx, cfg.dt, ri.COEFFS_F32, nsteps, sources=srcs, nthreads=cores)
-        return time.perf_counter() - t
+        return oracle.last_loop_seconds()
 
     for _ in range(args.warmup):
         one()
@@ -174,17 +196,17 @@ def run_reference(args):
     pts = v.size * nsteps
     val = pts * len(ts) / sum(ts) / 1e9
     sample = (f"first {planes} z-planes of C{cfg.k} ({cfg.nx}x{cfg.ny}x{planes}), "
-              f"{nsteps} time steps per bench step")
+              f"{nsteps} time steps per bench step, step loop only")
+    model, sockets = host_cpu()
     line = {"impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": "Gpoints/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * sum(ts) / len(ts), 3), "higher_is_better": True,
-            "scaling": "strong" if args.config in (3, 4) else "weak", "vs_baseline": None,
+            "scaling": "strong" if args.config in (1, 2, 3, 4) else "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (seeded, rtm_inputs)",
-            "config": {"workload": f"C{cfg.k}", "grid": [cfg.nx, cfg.ny, cfg.nz],
-                       "time_steps": cfg.steps, "sample": sample},
+            "config": bench_config(cfg, args.gpus, 1, args.halo, nsteps_cfg),
             "cpu_baseline": {"value": round(val, 4), "unit": "Gpoints/s", "cores": cores,
                              "kind": "oracle", "sample": sample,
-                             "cpu_model": host_cpu()[0], "sockets": host_cpu()[1]},
+                             "cpu_model": model, "sockets": sockets},
             "e2e": {"value": round(val, 4), "unit": "Gpoints/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -208,28 +230,23 @@ def host_cpu():
 
 
 def cpu_baseline(cfg, v_full):
-    """Oracle timed on the host cores on a bounded sample (~10 s) of the workload."""
+    """Oracle timed on the host cores on a bounded sample (~12 s) of the workload: the same
+    sample and the same clock (the oracle's step loop) as the --impl reference arm."""
     import oracle
     import rtm_inputs as ri
     cores = len(os.sched_getaffinity(0))
-    planes = max(10, min(cfg.nz, int(64 * (1024 * 1024) / (cfg.nx * cfg.ny))))
-    v = np.ascontiguousarray(v_full[:planes])
-    t = time.perf_counter()
-    oracle.run(v, cfg.dx, cfg.dt, ri.COEFFS_F32, 1, nthreads=cores)
-    t1 = time.perf_counter() - t
-    t = time.perf_counter()
-    oracle.run(v, cfg.dx, cfg.dt, ri.COEFFS_F32, 3, nthreads=cores)
-    per_step = max((time.perf_counter() - t - t1) / 2, 1e-3)  # marginal cost of a step
+    v, planes = oracle_sample(cfg, v_full, 64)
+    oracle.run(v, cfg.dx, cfg.dt, ri.COEFFS_F32, 2, nthreads=cores)
+    per_step = max(oracle.last_loop_seconds() / 2, 1e-3)
     n = int(max(1, min(200, 12.0 / per_step)))
-    t = time.perf_counter()
     oracle.run(v, cfg.dx, cfg.dt, ri.COEFFS_F32, n, nthreads=cores)
-    dt = time.perf_counter() - t
+    dt = oracle.last_loop_seconds()
     val = v.size * n / dt / 1e9
     model, sockets = host_cpu()
     return {"value": round(val, 4), "unit": "Gpoints/s", "cores": cores, "kind": "oracle",
             "cpu_model": model, "sockets": sockets,
             "sample": f"first {planes} z-planes of C{cfg.k} ({cfg.nx}x{cfg.ny}x{planes}), "
-                      f"{n} time steps, {dt:.1f} s"}
+                      f"{n} time steps, step loop only, {dt:.1f} s"}
 
 
 # ------------------------------------------------------------------------------ b200 arm
@@ -438,13 +455,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
             "higher_is_better": True, "scaling": "strong" if cfg.k in (1, 2, 3, 4) else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, rtm_inputs)",
-            "config": {"workload": wl, "grid": [cfg.nx, cfg.ny, cfg.nz], "time_steps": nsteps,
-                       "sources": len(cfg.sources_xyz), "shots": shots,
-                       "parallelism": f"z-slab x{world}",
-                       "halo": ("fused IPC push + flags" if args.halo == 2 else "NCCL send/recv")
-                       if world > 1 else None,
-                       "tile": tile_name, "l2": "inputs larger than L2 (3 x 4 GiB fields)"
-                       if pts_local * 4 > 126e6 else "L2-resident (no flush)"},
+            "config": bench_config(cfg, world, shots, args.halo, nsteps),
+            "kernel_variant": tile_name,
             "hbm_effective_gbs": round(value * bytes_per_pt, 1),
             "hbm_frac_of_8tbs": round(value * bytes_per_pt / 8000.0, 4),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None,

@@ -96,6 +96,12 @@ int rtm_set_fields(rtm_ctx* ctx, const float* u, const float* u_prev);
 int rtm_read_fields(rtm_ctx* ctx, float* u, float* u_prev);
 /* u = u_prev = 0 and step = 0; keeps velocity, sources and tile choice. */
 int rtm_reset(rtm_ctx* ctx);
+/* Extents of the host arrays this context reads and writes (host-only query, no device
+ * work): *nx, *ny, *nzl (this rank's / slab set's planes: nz for single-GPU, batched and
+ * multi-slab contexts, the slab's nzl for a distributed rank) and *nshots (1 unless batched).
+ * Field arrays hold nshots*nzl*ny*nx floats, the velocity nzl*ny*nx.  Any pointer may be
+ * NULL.  The Python binding validates every host array against it. */
+int rtm_get_dims(rtm_ctx* ctx, int* nx, int* ny, int* nzl, int* nshots);
 /* Number of steps taken since the last reset / set_fields. */
 long long rtm_step_count(rtm_ctx* ctx);
 /* Checkpoint / resume: after rtm_set_fields(u^n, u^{n-1}) of a saved state, set the step index

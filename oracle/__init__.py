@@ -45,6 +45,8 @@ def lib():
         L.oracle_points_f32.argtypes = [I, I, I, F, F, P, P, P, P, ctypes.c_long, P, P]
         L.oracle_slab_step_f32.argtypes = [I, I, I, P, P, P, P, I]
         L.oracle_cfield_f32.argtypes = [ctypes.c_long, F, F, P, P]
+        L.oracle_last_loop_seconds.argtypes = []
+        L.oracle_last_loop_seconds.restype = D
         for f in ("oracle_run_f32", "oracle_run_f64", "oracle_points_f32",
                   "oracle_slab_step_f32", "oracle_cfield_f32", "oracle_max_threads"):
             getattr(L, f).restype = I
@@ -125,3 +127,8 @@ def slab_step_f32(coeffs, C, U, P, nthreads=0):
 
 def max_threads() -> int:
     return int(lib().oracle_max_threads())
+
+
+def last_loop_seconds() -> float:
+    """Wall time of the step loop of the last ``run`` (allocation, C(p) and copies excluded)."""
+    return float(lib().oracle_last_loop_seconds())

@@ -31,6 +31,7 @@
 //  itself is not printed by the paper; every function below is pinned by closed forms,
 //  invariants or brute force as listed in DESIGN.md §"Oracle pins".
 // =====================================================================================
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -43,6 +44,10 @@
 namespace {
 
 constexpr int R = 5;  // stencil radius: "five points (cells) in each direction"
+
+// Wall time of the step loop of the last run() (set-up and copies excluded; SURVEY.md §8(d)
+// "time with a steady_clock around the step loop only").  Instrumentation, not arithmetic.
+double g_loop_seconds = 0.0;
 
 struct FtzGuard {  // FTZ/DAZ for this thread while alive (fp32 subnormal stalls)
     unsigned int saved;
@@ -113,6 +118,7 @@ int run(int nx, int ny, int nz, VT dx, VT dt, const T coeffs[6], const VT* v,
     T* Ua = U.a.data();
     T* Pa = P.a.data();
     const T* Ca = Cf.a.data();
+    const auto t_loop = std::chrono::steady_clock::now();
     for (int n = 0; n < steps; ++n) {
         T* N = Pa;  // N aliases P
 #pragma omp parallel for num_threads(nthreads) schedule(static)
@@ -131,6 +137,7 @@ int run(int nx, int ny, int nz, VT dx, VT dt, const T coeffs[6], const VT* v,
         }
         T* t = Pa; Pa = Ua; Ua = t;  // P <- U, U <- N
     }
+    g_loop_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_loop).count();
     for (int z = 0; z < nz; ++z)
         for (int y = 0; y < ny; ++y)
             for (int x = 0; x < nx; ++x) {
@@ -248,5 +255,8 @@ int oracle_cfield_f32(long n, float dx, float dt, const float* v, float* C) {
 }
 
 int oracle_max_threads(void) { return omp_get_max_threads(); }
+
+// Seconds spent in the step loop of the last oracle_run_f32/f64 call (bench timing only).
+double oracle_last_loop_seconds(void) { return g_loop_seconds; }
 
 }  // extern "C"

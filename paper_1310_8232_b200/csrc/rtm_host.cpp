@@ -82,7 +82,10 @@ struct Slab {
     size_t buf_planes() const { return (size_t)nshots * (nzl + 10); }
     float* C = nullptr;                  // nzl planes
     int* d_step = nullptr;               // [2]
-    unsigned int* d_stats = nullptr;     // [2] velocity check
+    unsigned int* d_stats = nullptr;     // [2] velocity check (also the deferred async verdict)
+    unsigned int* d_fstats = nullptr;    // [2] field check (rtm_field_stats): its own buffer, so a
+                                         // scan never overwrites a pending velocity verdict
+    int tb_nbands = -1;                  // band count of the last two-step plan (flags reset on change)
     float* d_samples = nullptr;
     std::vector<DevSource> srcs;
     std::vector<float> h_samples;
@@ -255,6 +258,7 @@ int alloc_slab(rtm_ctx* c, Slab& s) {
     }
     CK(cudaMalloc(&s.d_step, 2 * sizeof(int)));
     CK(cudaMalloc(&s.d_stats, 2 * sizeof(unsigned int)));
+    CK(cudaMalloc(&s.d_fstats, 2 * sizeof(unsigned int)));
     CK(cudaStreamCreateWithFlags(&s.s_own, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&s.s_comm, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&s.ev_bnd, cudaEventDisableTiming));
@@ -285,6 +289,7 @@ void free_slab(Slab& s) {
     if (s.C) cudaFree(s.C);
     if (s.d_step) cudaFree(s.d_step);
     if (s.d_stats) cudaFree(s.d_stats);
+    if (s.d_fstats) cudaFree(s.d_fstats);
     if (s.d_samples) cudaFree(s.d_samples);
     if (s.ev_bnd) cudaEventDestroy(s.ev_bnd);
     if (s.ev_comm) cudaEventDestroy(s.ev_comm);
@@ -659,6 +664,13 @@ int tb_pass(rtm_ctx* c, Slab& s, int parity, cudaStream_t st) {
     q.flagsB = s.d_flags + c->num_sms;
     q.d_epoch = s.d_epoch;
     q.nbands = (int)bands.size();
+    if (s.tb_nbands != q.nbands) {
+        // the flag epoch E = (epoch * nbands + band + 1) << 32 only grows while nbands is fixed:
+        // a new plan (RTM_OPT_TB_CTAS, tile) starts from cleared flags so no stale value can
+        // satisfy a >= wait of the new numbering
+        CK(cudaMemsetAsync(s.d_flags, 0, 2 * (size_t)c->num_sms * sizeof(unsigned long long), st));
+        s.tb_nbands = q.nbands;
+    }
     q.tiles_x = tiles_x;
     q.nsrc = (int)s.srcs.size();
     for (int k = 0; k < q.nsrc; ++k) q.src[k] = s.srcs[k];
@@ -1073,6 +1085,20 @@ int step_slabs(rtm_ctx* c, int nsteps) {
     return RTM_OK;
 }
 
+// Barrier across the ranks of a distributed context (NCCL all-reduce of one value, then a
+// stream synchronisation): on return every rank has reached this call.
+int comm_barrier(rtm_ctx* c) {
+    Slab& s = c->slabs[0];
+    CK(cudaSetDevice(s.dev));
+    double* d = nullptr;
+    CK(cudaMalloc(&d, sizeof(double)));
+    const ncclResult_t nr = ncclAllReduce(d, d, 1, ncclFloat64, ncclSum, c->comm, s.stream());
+    const cudaError_t e = cudaStreamSynchronize(s.stream());
+    cudaFree(d);
+    if (nr != ncclSuccess || e != cudaSuccess) return fail(RTM_ENCCL, "rank barrier failed");
+    return RTM_OK;
+}
+
 int sync_all(rtm_ctx* c) {
     for (auto& s : c->slabs) {
         CK(cudaSetDevice(s.dev));
@@ -1171,16 +1197,20 @@ int reset_impl(rtm_ctx* c, const float* u, const float* up) {
     c->step = 0;
     ++c->sig_gen;  // synchronising (halo exchange + sync below): flags restart
     c->sig_fresh = true;
-    // G > 1: fill the halo planes of u^0 and u^{-1} from the neighbours' initial data
+    // G > 1: fill the halo planes of u^0 from the neighbours' initial data.  Only u^0: the
+    // stencil reads u^{-1} at owned points only, so the halo planes of buf[1] are never read
+    // before step 0 overwrites them (its exchange or fused push).  Not exchanging them also
+    // keeps the first (wait-free) fused-push step of a generation race-free across ranks: the
+    // only remote write into this slab's buf[1] halo planes is then the neighbour's push, and
+    // the neighbour can only push after this exchange, i.e. after this rank's reset memsets
+    // (stream order on the sending side of the exchange).
     if (c->slabs.size() > 1 || c->mode == 2) {
-        for (int par = 0; par < 2; ++par) {
-            for (auto& s : c->slabs) {
-                CK(cudaSetDevice(s.dev));
-                CK(cudaEventRecord(s.ev_bnd, s.stream()));
-            }
-            if (c->mode == 2) RET(exchange_nccl(c, par));
-            else RET(exchange_local(c, par));
+        for (auto& s : c->slabs) {
+            CK(cudaSetDevice(s.dev));
+            CK(cudaEventRecord(s.ev_bnd, s.stream()));
         }
+        if (c->mode == 2) RET(exchange_nccl(c, 0));
+        else RET(exchange_local(c, 0));
     }
     return sync_all(c);
 }
@@ -1603,6 +1633,15 @@ int rtm_reset(rtm_ctx* c) {
 
 long long rtm_step_count(rtm_ctx* c) { return c ? c->step : -1; }
 
+int rtm_get_dims(rtm_ctx* c, int* nx, int* ny, int* nzl, int* nshots) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    if (nx) *nx = c->nx;
+    if (ny) *ny = c->ny;
+    if (nzl) *nzl = c->mode == 2 ? c->slabs[0].nzl : c->nz;
+    if (nshots) *nshots = c->slabs[0].nshots;
+    return RTM_OK;
+}
+
 int rtm_set_step_count(rtm_ctx* c, long long n) {
     if (!c) return fail(RTM_EINVAL, "ctx is NULL");
     if (n < 0 || n > (1LL << 30)) return fail(RTM_EINVAL, "step index %lld out of range", n);
@@ -1626,16 +1665,7 @@ int rtm_set_step_count(rtm_ctx* c, long long n) {
     }
     c->step = n;
     if (c->halo_mode == 2) {  // flags restart: make the call collective across ranks
-        if (c->comm) {
-            Slab& s = c->slabs[0];
-            CK(cudaSetDevice(s.dev));
-            double* d = nullptr;
-            CK(cudaMalloc(&d, sizeof(double)));
-            const ncclResult_t nr = ncclAllReduce(d, d, 1, ncclFloat64, ncclSum, c->comm, s.stream());
-            const cudaError_t e = cudaStreamSynchronize(s.stream());
-            cudaFree(d);
-            if (nr != ncclSuccess || e != cudaSuccess) return fail(RTM_ENCCL, "set_step_count barrier failed");
-        }
+        if (c->comm) RET(comm_barrier(c));
         ++c->sig_gen;
         c->sig_fresh = true;
     }
@@ -1650,10 +1680,10 @@ int rtm_field_stats(rtm_ctx* c, double* max_abs, long long* nonfinite) {
     long long bad = 0;
     for (auto& s : c->slabs) {
         CK(cudaSetDevice(s.dev));
-        CK(cudaMemsetAsync(s.d_stats, 0, 2 * sizeof(unsigned int), s.stream()));
-        CK(launch_field_stats(s.buf[c->step & 1], plane, s.nzl, s.nshots, s.d_stats, s.stream()));
+        CK(cudaMemsetAsync(s.d_fstats, 0, 2 * sizeof(unsigned int), s.stream()));
+        CK(launch_field_stats(s.buf[c->step & 1], plane, s.nzl, s.nshots, s.d_fstats, s.stream()));
         unsigned int h[2];
-        CK(cudaMemcpyAsync(h, s.d_stats, sizeof h, cudaMemcpyDeviceToHost, s.stream()));
+        CK(cudaMemcpyAsync(h, s.d_fstats, sizeof h, cudaMemcpyDeviceToHost, s.stream()));
         CK(cudaStreamSynchronize(s.stream()));
         float f;
         std::memcpy(&f, &h[0], 4);
@@ -1905,6 +1935,16 @@ int rtm_autotune(rtm_ctx* c, int nI, const int* tiles, const int* zchunks, int n
     }
     c->step = saved_step;
     cleanup();
+    if (c->halo_mode == 2) {
+        // The flag words hold g|(steps reached while tuning), beyond every later target g|n:
+        // start a new generation so the waits order the slabs again.  Across ranks the restore
+        // must also be complete everywhere before anyone pushes into a neighbour's halo: the
+        // timed phases end in an all-reduce (all ranks' tuning steps done), and this barrier
+        // orders every rank's restore before the next step of any rank.
+        if (c->comm && rc == RTM_OK) rc = comm_barrier(c);
+        ++c->sig_gen;
+        c->sig_fresh = true;
+    }
     if (rc != RTM_OK) {
         c->tile = saved_tile;
         c->zchunk = saved_zc;

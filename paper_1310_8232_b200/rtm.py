@@ -56,6 +56,8 @@ _SIGS = {
     "rtm_read_fields": (_I, [_P, _P, _P]),
     "rtm_reset": (_I, [_P]),
     "rtm_step_count": (_LL, [_P]),
+    "rtm_get_dims": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I), ctypes.POINTER(_I),
+                         ctypes.POINTER(_I)]),
     "rtm_set_step_count": (_I, [_P, _LL]),
     "rtm_field_stats": (_I, [_P, ctypes.POINTER(_D), ctypes.POINTER(_LL)]),
     "rtm_set_velocity_device": (_I, [_P, _P]),
@@ -113,6 +115,37 @@ def _f32(a, n=None, name="array"):
     return a
 
 
+def rtm_get_dims(h):
+    """(nx, ny, nzl, nshots) of the host arrays the context reads and writes."""
+    nx, ny, nzl, ns = _I(0), _I(0), _I(0), _I(0)
+    _check(lib.rtm_get_dims(h, ctypes.byref(nx), ctypes.byref(ny), ctypes.byref(nzl),
+                            ctypes.byref(ns)))
+    return int(nx.value), int(ny.value), int(nzl.value), int(ns.value)
+
+
+def _n_velocity(h):
+    nx, ny, nzl, _ = rtm_get_dims(h)
+    return nx * ny * nzl
+
+
+def _n_field(h):
+    nx, ny, nzl, ns = rtm_get_dims(h)
+    return nx * ny * nzl * ns
+
+
+def _out_buf(a, h, name):
+    """A host output array the library writes the context's field into: it must be exactly
+    that (float32, C-contiguous, writeable, nshots*nzl*ny*nx elements)."""
+    if not isinstance(a, np.ndarray):
+        raise ValueError(f"{name} must be a numpy array")
+    if a.dtype != np.float32 or not a.flags.c_contiguous or not a.flags.writeable:
+        raise ValueError(f"{name} must be a writeable C-contiguous float32 array")
+    n = _n_field(h)
+    if a.size != n:
+        raise ValueError(f"{name} has {a.size} elements, expected {n}")
+    return _ptr(a)
+
+
 def _ptr(a):
     return None if a is None else a.ctypes.data_as(_P)
 
@@ -134,7 +167,7 @@ def rtm_create(nx, ny, nz, dx, dt, coeffs):
 
 
 def rtm_set_velocity(h, v, n=None):
-    v = _f32(v, n, "v")
+    v = _f32(v, _n_velocity(h), "v")
     return _check(lib.rtm_set_velocity(h, _ptr(v)))
 
 
@@ -149,8 +182,7 @@ def rtm_step(h, nsteps):
 
 
 def rtm_read_field(h, out):
-    assert out.dtype == np.float32 and out.flags.c_contiguous
-    return _check(lib.rtm_read_field(h, _ptr(out)))
+    return _check(lib.rtm_read_field(h, _out_buf(out, h, "out")))
 
 
 def rtm_destroy(h):
@@ -164,13 +196,16 @@ def rtm_last_error() -> str:
 
 # ---- extensions --------------------------------------------------------------------------
 def rtm_set_fields(h, u=None, u_prev=None):
-    u = None if u is None else _f32(u)
-    up = None if u_prev is None else _f32(u_prev)
+    n = _n_field(h)
+    u = None if u is None else _f32(u, n, "u")
+    up = None if u_prev is None else _f32(u_prev, n, "u_prev")
     return _check(lib.rtm_set_fields(h, _ptr(u), _ptr(up)))
 
 
 def rtm_read_fields(h, u=None, u_prev=None):
-    return _check(lib.rtm_read_fields(h, _ptr(u), _ptr(u_prev)))
+    pu = None if u is None else _out_buf(u, h, "u")
+    pp = None if u_prev is None else _out_buf(u_prev, h, "u_prev")
+    return _check(lib.rtm_read_fields(h, pu, pp))
 
 
 def rtm_reset(h):
@@ -191,12 +226,15 @@ def rtm_field_stats(h):
     return float(m.value), int(bad.value)
 
 
-def _async_buf(a, name, write=False):
+def _async_buf(a, name, h, nfn, write=False):
     # no implicit conversion copy: the library reads/writes the caller's memory after return
     if not (isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags.c_contiguous
             and (a.flags.writeable or not write)):
         raise ValueError(f"{name} must be a C-contiguous float32 array"
                          + (" (writeable)" if write else ""))
+    n = nfn(h)  # the context's extents (raises RtmError for a NULL context)
+    if a.size != n:
+        raise ValueError(f"{name} has {a.size} elements, expected {n}")
     return _ptr(a)
 
 
@@ -211,7 +249,7 @@ def rtm_blocksize_lattice(S, P) -> list[int]:
 
 def rtm_set_velocity_async(h, v):
     """v must stay alive and unmodified until rtm_sync (keep a reference)."""
-    return _check(lib.rtm_set_velocity_async(h, _async_buf(v, "v")))
+    return _check(lib.rtm_set_velocity_async(h, _async_buf(v, "v", h, _n_velocity)))
 
 
 def rtm_step_async(h, nsteps):
@@ -220,7 +258,7 @@ def rtm_step_async(h, nsteps):
 
 def rtm_read_field_async(h, out):
     """out: a C-contiguous float32 array, filled once rtm_sync returns."""
-    return _check(lib.rtm_read_field_async(h, _async_buf(out, "out", write=True)))
+    return _check(lib.rtm_read_field_async(h, _async_buf(out, "out", h, _n_field, write=True)))
 
 
 def rtm_sync(h):

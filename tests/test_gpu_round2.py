@@ -1,0 +1,154 @@
+"""GPU regression tests of round 2: state restarts of the fused-halo flag protocol and the
+two-step flag numbering, the field check's own reduction buffer, and host-array validation in
+the binding.  Each compares against the G = 1 single-step kernel bitwise (R14, SURVEY.md §8(c)
+P11) or checks an error contract of include/rtm.h."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import rtm_inputs as ri
+
+pytestmark = pytest.mark.gpu
+C32 = ri.COEFFS_F32
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from conftest import build_library
+    build_library()
+    import paper_1310_8232_b200 as P
+    return P
+
+
+def _single(P, v, steps, u0, up0, src, tile=35):
+    nz, ny, nx = v.shape
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32) as sim:
+        sim.set_tile(tile)
+        sim.set_velocity(v)
+        for s in src:
+            sim.inject_source(*s)
+        sim.set_fields(u0, up0)
+        sim.step(steps)
+        return sim.read_fields()
+
+
+def _case(seed, shape=(47, 33, 72)):
+    rng = np.random.default_rng(seed)
+    v = rng.uniform(1500, 4300, shape).astype(np.float32)
+    u0, up0 = ri.random_fields(shape, seed=seed + 1)
+    w = ri.source_samples(2500.0, 1e-3, 15.0, 40)
+    nz = shape[0]
+    src = [(5, 6, nz // 3, w), (7, 8, 2 * nz // 3 - 1, -w), (1, 1, 0, w)]
+    return v, u0, up0, src
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_autotune_then_step_in_halo_mode_2_is_bitwise(P, G):
+    """rtm_autotune rewinds the step counter; the flag words then hold
+    generation|steps-reached-while-tuning.  The tuner now starts a new flag generation (after a
+    rank barrier in distributed contexts), so the slabs stay ordered after tuning."""
+    v, u0, up0, src = _case(10 + G)
+    ref_u, ref_up = _single(P, v, 17, u0, up0, src)
+    nz, ny, nx = v.shape
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, devices=[0] * G) as sim:
+        P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, 2)
+        sim.set_velocity(v)
+        for s in src:
+            sim.inject_source(*s)
+        sim.set_fields(u0, up0)
+        sim.step(5)
+        res, _ = P.rtm_autotune(sim.h, 6, tiles=[1, 35, 8], zchunks=[0, 0, 9])
+        assert sim.steps_taken == 5
+        sim.step(12)
+        u, up = sim.read_fields()
+    assert np.array_equal(u, ref_u) and np.array_equal(up, ref_up)
+
+
+def test_field_stats_keeps_the_pending_async_velocity_verdict(P):
+    """rtm_field_stats between rtm_set_velocity_async and rtm_sync must not
+    overwrite the deferred CFL verdict (it now reduces into its own buffer)."""
+    shape = (20, 24, 32)
+    good = np.full(shape, 2000.0, np.float32)
+    bad = np.full(shape, 2000.0, np.float32)
+    bad[3, 4, 5] = 9000.0  # nu = 0.9 > nu_crit
+    with P.Simulation(shape[2], shape[1], shape[0], 10.0, 1e-3, C32) as sim:
+        sim.set_velocity(good)
+        sim.set_fields(*ri.random_fields(shape, seed=5))
+        P.rtm_set_velocity_async(sim.h, bad)
+        m, nbad = P.rtm_field_stats(sim.h)
+        assert m > 0 and nbad == 0
+        with pytest.raises(P.RtmError) as e:
+            P.rtm_sync(sim.h)
+        assert e.value.code == P.RTM_ECFL
+        # the verdict marked the velocity unset
+        with pytest.raises(P.RtmError) as e:
+            sim.step(1)
+        assert e.value.code == P.RTM_ESTATE
+
+
+def test_two_step_plan_change_on_a_running_context_is_bitwise(P):
+    """the two-step flag epoch (epoch*nbands + band + 1) only grows while
+    the band count is fixed.  Raising RTM_OPT_TB_CTAS on a context that already ran passes
+    lowers the band count; the flags are now cleared when the plan changes."""
+    shape = (23, 150, 200)
+    v, u0, up0, src = _case(77, shape)
+    ref_u, ref_up = _single(P, v, 30, u0, up0, src)
+    tb = [t for t in range(P.rtm_num_tiles()) if (P.rtm_tile_name(t) or "").startswith("tb2")]
+    nz, ny, nx = shape
+    for t in (tb[0], tb[-1]):
+        with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32) as sim:
+            sim.set_tile(t)
+            sim.set_velocity(v)
+            for s in src:
+                sim.inject_source(*s)
+            sim.set_fields(u0, up0)
+            P.rtm_set_option(sim.h, P.RTM_OPT_GRAPHS, 0)
+            P.rtm_set_option(sim.h, P.RTM_OPT_TB_CTAS, 12)   # many narrow bands
+            sim.step(10)
+            P.rtm_set_option(sim.h, P.RTM_OPT_TB_CTAS, 0)    # one band per SM set: fewer bands
+            sim.step(10)
+            P.rtm_set_option(sim.h, P.RTM_OPT_TB_CTAS, 24)
+            P.rtm_set_option(sim.h, P.RTM_OPT_GRAPHS, 1)
+            sim.step(10)
+            u, up = sim.read_fields()
+        assert np.array_equal(u, ref_u), P.rtm_tile_name(t)
+        assert np.array_equal(up, ref_up), P.rtm_tile_name(t)
+
+
+def test_binding_validates_host_arrays(P):
+    """every host-array entry point checks dtype, contiguity and element count
+    against the context's extents (rtm_get_dims) and raises ValueError before the library
+    touches memory."""
+    shape = (12, 10, 16)
+    v = np.full(shape, 2000.0, np.float32)
+    with P.Simulation(shape[2], shape[1], shape[0], 10.0, 1e-3, C32) as sim:
+        assert P.rtm_get_dims(sim.h) == (16, 10, 12, 1)
+        with pytest.raises(ValueError):
+            P.rtm_set_velocity(sim.h, v[:-1])
+        sim.set_velocity(v)
+        with pytest.raises(ValueError):
+            P.rtm_set_fields(sim.h, np.zeros(5, np.float32))
+        with pytest.raises(ValueError):
+            P.rtm_read_field(sim.h, np.empty(shape[0] * shape[1] * shape[2] - 1, np.float32))
+        with pytest.raises(ValueError):
+            P.rtm_read_field(sim.h, np.empty(shape, np.float64))
+        with pytest.raises(ValueError):
+            P.rtm_read_field(sim.h, np.empty((shape[0], shape[1], 2 * shape[2]), np.float32)[:, :, ::2])
+        with pytest.raises(ValueError):
+            P.rtm_read_fields(sim.h, None, np.empty(7, np.float32))
+        with pytest.raises(ValueError):
+            P.rtm_read_field_async(sim.h, np.empty(9, np.float32))
+        with pytest.raises(ValueError):
+            P.rtm_set_velocity_async(sim.h, np.ones(9, np.float32))
+        out = np.empty(shape, np.float32)
+        P.rtm_read_field(sim.h, out)  # the exact shape still works
+    with P.Simulation(16, 10, 12, 10.0, 1e-3, C32, shots=3) as sim:
+        assert P.rtm_get_dims(sim.h) == (16, 10, 12, 3)
+        sim.set_velocity(v)
+        with pytest.raises(ValueError):
+            P.rtm_read_field(sim.h, np.empty(shape, np.float32))
+        assert sim.read_field().shape == (3,) + shape
