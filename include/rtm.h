@@ -181,7 +181,23 @@ const char* rtm_tile_name(int tile_id);  /* e.g. "stream64x32k10d0"; NULL for un
  *                        flags are CUDA-IPC mappings (same node, peer access) set up by an NCCL
  *                        all-gather of the handles: setting it there is a COLLECTIVE call, as is
  *                        rtm_set_step_count while it is active.  Needs 64-bit stream memory ops.
+ *                      3 copy-engine pull ordered by the flag protocol (SURVEY §8(e) "SM-free
+ *                        alternative"): after its boundary planes each slab releases "boundary n
+ *                        ready" into the neighbours' flag words; a neighbour's comm stream waits
+ *                        on it and PULLS the 5 planes with cudaMemcpyAsync from the (peer /
+ *                        CUDA-IPC mapped) buffer into its own halo, overlapped with its interior
+ *                        kernel — no NCCL kernels, no SM time for the transfer, and every rank
+ *                        writes only its own memory.  In-process or across processes (IPC); the
+ *                        default of peer contexts (rtm_create_peer).
  *                      Peer access is required between neighbouring devices (else RTM_EINVAL).
+ *                      Setting 2 or 3 in a distributed context is a COLLECTIVE call.
+ *   RTM_OPT_HOST_ORDERED 1: before every device-side flag wait of halo modes 2/3 the library
+ *                      synchronises its streams and calls the rank barrier (the NCCL
+ *                      communicator or the rtm_set_host_barrier callback), so every wait is
+ *                      already satisfied when it is enqueued.  This runs the cross-process data
+ *                      plane with host ordering only — used to test several ranks on ONE GPU,
+ *                      where device-side waits between processes are not allowed — at the cost
+ *                      of one host barrier per step.  0 (default): device-ordered.
  *   RTM_OPT_TB_CTAS    two-step variants ("tb2_*"): max CTAs per y-band launch,
  *                      0 (default) = one per SM.  Smaller values force more, narrower bands
  *                      (used by the tests to cover band edges on small grids).
@@ -190,7 +206,8 @@ const char* rtm_tile_name(int tile_id);  /* e.g. "stream64x32k10d0"; NULL for un
  *                      wait on griddepcontrol.wait before touching memory); 0: plain launches.
  * Unknown key or out-of-range value -> RTM_EINVAL.  rtm_get_option returns -1 for unknown keys. */
 enum { RTM_OPT_ZCHUNK = 1, RTM_OPT_CACHE_MODE = 2, RTM_OPT_GRAPHS = 3, RTM_OPT_SHOT_ORDER = 4,
-       RTM_OPT_HALO_MODE = 5, RTM_OPT_CHECK_EVERY = 6, RTM_OPT_TB_CTAS = 7, RTM_OPT_PDL = 8 };
+       RTM_OPT_HALO_MODE = 5, RTM_OPT_CHECK_EVERY = 6, RTM_OPT_TB_CTAS = 7, RTM_OPT_PDL = 8,
+       RTM_OPT_HOST_ORDERED = 9 };
 int rtm_set_option(rtm_ctx* ctx, int key, long long value);
 long long rtm_get_option(rtm_ctx* ctx, int key);
 
@@ -278,6 +295,37 @@ int rtm_get_unique_id(unsigned char id[128]);
 rtm_ctx* rtm_create_dist(int nx, int ny, int nz_global, float dx, float dt,
                          const float coeffs[6], int rank, int world, const unsigned char id[128],
                          int device);
+
+/* One process per GPU WITHOUT NCCL (peer context): the same z-slab of rank `rank` as
+ * rtm_create_dist, on CUDA device `device`, whose neighbours are reached only through CUDA-IPC
+ * mappings.  Bootstrap (any out-of-band channel, e.g. a torch.distributed gloo group):
+ *   1. every rank calls rtm_ipc_export and sends its record to its neighbours;
+ *   2. every rank calls rtm_ipc_import with the records of rank-1 and rank+1 (NULL where absent);
+ *   3. every rank installs a rank barrier with rtm_set_host_barrier.
+ * The default halo mode is 3 (copy-engine pull); 2 (fused push) is also available; 0 (NCCL)
+ * is not (RTM_EINVAL).  rtm_reset / rtm_set_fields / rtm_set_step_count / rtm_set_option(
+ * RTM_OPT_HALO_MODE) / rtm_autotune are collective (they call the barrier); rtm_step before the
+ * import -> RTM_ESTATE.  Ranks may share a device (each then maps the others' buffers). */
+rtm_ctx* rtm_create_peer(int nx, int ny, int nz_global, float dx, float dt, const float coeffs[6],
+                         int rank, int world, int device);
+
+/* The 512-byte CUDA-IPC record of a slab context (peer or NCCL-distributed): IPC handles of
+ * its two time-level buffers and of its flag words, plus the grid extents, rank and world it
+ * belongs to (checked on import).  Plain bytes: send them over any channel. */
+#define RTM_IPC_RECORD_BYTES 512
+int rtm_ipc_export(rtm_ctx* ctx, unsigned char rec[RTM_IPC_RECORD_BYTES]);
+/* Open the neighbours' records (lo = rank-1, hi = rank+1; NULL for an absent neighbour).
+ * RTM_EINVAL if a record belongs to another grid / world / rank, or a neighbour that exists is
+ * passed NULL; RTM_ECUDA if a handle cannot be opened.  May be called once per context. */
+int rtm_ipc_import(rtm_ctx* ctx, const unsigned char* lo, const unsigned char* hi);
+/* Rank barrier of a peer context: fn(user) must return 0 once every rank of the context has
+ * called it (non-zero aborts the calling operation with RTM_ESTATE).  Called from the thread
+ * that calls the library.  fn = NULL removes it. */
+typedef int (*rtm_barrier_fn)(void* user);
+int rtm_set_host_barrier(rtm_ctx* ctx, rtm_barrier_fn fn, void* user);
+/* Host time (ms) the last rtm_step spent enqueuing work (launches, waits, copies, graph
+ * launches), excluding its final synchronisation; divide by the steps for a per-step cost. */
+double rtm_last_enqueue_ms(rtm_ctx* ctx);
 
 /* Host-only plan helpers (no GPU needed; shared by the library and the CPU tests).
  * rtm_slab_range: rank's owned global planes [*z0, *z0 + *nzl); balanced split

@@ -10,9 +10,11 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -112,12 +114,14 @@ struct Slab {
     int tb_graph_variant[4] = {-1, -1, -1, -1};
     // fused halo push with the flag protocol (halo mode 2): the neighbours' time-level buffers
     // and flag words — direct pointers in-process, CUDA-IPC mappings across processes
-    unsigned long long* d_sig = nullptr;       // [2]: steps completed by the lo / hi neighbour
+    unsigned long long* d_sig = nullptr;       // [4]: steps completed by the lo / hi neighbour
+                                               // ([0] / [1], mode 2), boundary of step n ready
+                                               // at the lo / hi neighbour ([2] / [3], mode 3)
     float* nb_lo[2] = {nullptr, nullptr};
     float* nb_hi[2] = {nullptr, nullptr};
     int nb_lo_nzl = 0;
-    unsigned long long* nb_lo_sig = nullptr;   // the lo neighbour's d_sig (we write its [1])
-    unsigned long long* nb_hi_sig = nullptr;   // the hi neighbour's d_sig (we write its [0])
+    unsigned long long* nb_lo_sig = nullptr;   // the lo neighbour's d_sig (we write its [1] / [3])
+    unsigned long long* nb_hi_sig = nullptr;   // the hi neighbour's d_sig (we write its [0] / [2])
     std::vector<void*> ipc_open;               // mappings to cudaIpcCloseMemHandle
     cudaStream_t stream() const { return has_user ? s_user : s_own; }
 };
@@ -125,7 +129,7 @@ struct Slab {
 }  // namespace
 
 struct rtm_ctx {
-    int mode = 0;  // 0 single, 1 multi (in-process slabs), 2 dist (NCCL)
+    int mode = 0;  // 0 single, 1 multi (in-process slabs), 2 dist (NCCL), 3 peer (CUDA IPC, no NCCL)
     int nx = 0, ny = 0, nz = 0;  // nz = global planes
     int px = 0;                  // device row pitch in floats: nx rounded up to a multiple of 4
     float dx = 0, dt = 0;
@@ -141,7 +145,14 @@ struct rtm_ctx {
     int cache_mode = 0x45;  // u box TMA evict_last (+0.8 % on C4, profiles/sweep_cache_r01h.log); D=0 variants: L2 prefetch of u_prev/C 4 planes ahead, evict_last
     int shot_order = 0;     // 0 auto, 1 shot-major, 2 shot-fastest
     int halo_mode = 0;      // slabs: 0 boundary first + copies / NCCL, 1 fused push (events,
-                            // in-process), 2 fused push + flag protocol (in-process or IPC)
+                            // in-process), 2 fused push + flag protocol (in-process or IPC),
+                            // 3 copy-engine pull + flag protocol (in-process or IPC)
+    bool host_ordered = false;       // RTM_OPT_HOST_ORDERED: rank barrier before flag waits
+    bool ipc_imported = false;       // peer / dist contexts: neighbours' records opened
+    rtm_barrier_fn barrier_fn = nullptr;  // peer contexts: the caller's rank barrier
+    void* barrier_user = nullptr;
+    double enqueue_ms = 0;           // host enqueue time of the last rtm_step
+    bool slab_graphs_broken = false; // capture of the slab step failed once: direct launches
     unsigned long long sig_gen = 0;  // flag generation (bumped at every synchronising reset)
     bool sig_fresh = true;           // first step of a generation: no flag waits
     unsigned sig_flush = 0;          // CU_STREAM_WAIT_VALUE_FLUSH when the devices support it
@@ -184,7 +195,6 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-typedef CUresult (*PFN_waitv64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
 typedef CUresult (*PFN_devattr)(int*, CUdevice_attribute, CUdevice);
 template <class F>
 F driver_fn(const char* name) {
@@ -836,13 +846,13 @@ int exchange_local(rtm_ctx* c, int parity_next) {
         float* dst = s.buf[parity_next];
         if (s.lo_nb) {
             const Slab& n = c->slabs[r - 1];
-            CK(cudaMemcpyPeerAsync(dst, s.dev, n.buf[parity_next] + (size_t)n.nzl * plane, n.dev,
-                                   bytes, s.s_comm));
+            CK(cudaMemcpyAsync(dst, n.buf[parity_next] + (size_t)n.nzl * plane, bytes,
+                               cudaMemcpyDefault, s.s_comm));  // peer copy through UVA (capturable)
         }
         if (s.hi_nb) {
             const Slab& n = c->slabs[r + 1];
-            CK(cudaMemcpyPeerAsync(dst + (size_t)(s.nzl + 5) * plane, s.dev,
-                                   n.buf[parity_next] + 5 * plane, n.dev, bytes, s.s_comm));
+            CK(cudaMemcpyAsync(dst + (size_t)(s.nzl + 5) * plane, n.buf[parity_next] + 5 * plane,
+                               bytes, cudaMemcpyDefault, s.s_comm));
         }
         CK(cudaEventRecord(s.ev_comm, s.s_comm));
     }
@@ -870,54 +880,131 @@ int exchange_nccl(rtm_ctx* c, int parity_next) {
     return RTM_OK;
 }
 
-// G > 1 step, fused halo push (f1): one launch per slab per step whose epilogue also stores
-// the boundary planes into the neighbours' z-halo (peer stores over NVLink between GPUs, plain
-// stores on one GPU).  Step n on slab r waits for step n-1 of r-1, r, r+1 to finish: their
-// pushes into r's halo (RAW) and their reads of the halo planes r is about to overwrite (WAR).
-int step_slabs_fused(rtm_ctx* c, int nsteps) {
-    const int G = (int)c->slabs.size();
-    const size_t plane = dplane(c);
-    for (int k = 0; k < nsteps; ++k) {
-        const int parity = (int)(c->step & 1);
-        for (int r = 0; r < G; ++r) {
-            Slab& s = c->slabs[r];
-            CK(cudaSetDevice(s.dev));
-            for (int d = -1; d <= 1; d += 2)
-                if (r + d >= 0 && r + d < G) CK(cudaStreamWaitEvent(s.stream(), c->slabs[r + d].ev_done, 0));
-        }
-        for (int r = 0; r < G; ++r) {
-            Slab& s = c->slabs[r];
-            CK(cudaSetDevice(s.dev));
-            float* lo = s.lo_nb ? c->slabs[r - 1].buf[parity ^ 1] + (size_t)(c->slabs[r - 1].nzl + 5) * plane
-                                : nullptr;
-            float* hi = s.hi_nb ? c->slabs[r + 1].buf[parity ^ 1] : nullptr;
-            RET(launch_stencil(c, s, parity, 0, s.nzl, 0, 0, 1, s.stream(), lo, hi));
-            CK(cudaEventRecord(s.ev_done, s.stream()));
-        }
-        ++c->step;
-    }
-    for (int r = 0; r < G; ++r) {  // join: every push into r has landed when the step returns
-        Slab& s = c->slabs[r];
+// ---- rank synchronisation -------------------------------------------------------------
+// Barrier across the ranks of a distributed context: the NCCL communicator (all-reduce of one
+// value, then a stream synchronisation) or, for a peer context, the caller's host barrier.
+// In-process and single contexts have nothing to wait for.  On return every rank reached it.
+int ranks_barrier(rtm_ctx* c) {
+    if (c->comm) {
+        Slab& s = c->slabs[0];
         CK(cudaSetDevice(s.dev));
-        for (int d = -1; d <= 1; d += 2)
-            if (r + d >= 0 && r + d < G) CK(cudaStreamWaitEvent(s.stream(), c->slabs[r + d].ev_done, 0));
+        double* d = nullptr;
+        CK(cudaMalloc(&d, sizeof(double)));
+        const ncclResult_t nr = ncclAllReduce(d, d, 1, ncclFloat64, ncclSum, c->comm, s.stream());
+        const cudaError_t e = cudaStreamSynchronize(s.stream());
+        cudaFree(d);
+        if (nr != ncclSuccess || e != cudaSuccess) return fail(RTM_ENCCL, "rank barrier failed");
+        return RTM_OK;
+    }
+    if (c->mode == 3 && c->world > 1) {
+        if (!c->barrier_fn)
+            return fail(RTM_ESTATE, "peer context: this call is collective and needs rtm_set_host_barrier");
+        if (c->barrier_fn(c->barrier_user) != 0) return fail(RTM_ESTATE, "the host barrier callback failed");
     }
     return RTM_OK;
 }
 
-// Halo mode 2 set-up: flag words per slab, neighbours' buffer / flag pointers.  In-process
-// (mode 1) they are the other slabs' allocations; across processes (mode 2, one rank per GPU)
-// every rank exports CUDA-IPC handles of its two time-level buffers and its flag words, the
-// handles are all-gathered over the context's NCCL communicator (a collective call) and the
-// neighbours' are opened (cudaIpcMemLazyEnablePeerAccess: NVLink peer mappings).
+// ---- CUDA-IPC records (peer contexts; NCCL-distributed contexts in halo modes 2-3) -------
+// Every rank exports IPC handles of its two time-level buffers and its flag words; a
+// neighbour opens them (cudaIpcMemLazyEnablePeerAccess: NVLink peer mappings between GPUs,
+// plain mappings when the ranks share a device).
+constexpr unsigned kIpcMagic = 0x52544d31u;  // "RTM1"
 struct IpcRecord {
+    unsigned magic;
+    int version;
+    int rank, world;
+    int nx, ny, nz, nzl;
+    int device;
+    int pad0[7];
     cudaIpcMemHandle_t buf[2];
     cudaIpcMemHandle_t sig;
-    int nzl;
-    int pad[15];
+    unsigned char pad1[RTM_IPC_RECORD_BYTES - 64 - 3 * sizeof(cudaIpcMemHandle_t)];
 };
-static_assert(sizeof(IpcRecord) == 256, "IPC record size");
+static_assert(sizeof(IpcRecord) == RTM_IPC_RECORD_BYTES, "IPC record size");
 
+int alloc_sig(Slab& s) {
+    CK(cudaSetDevice(s.dev));
+    if (!s.d_sig) {
+        CK(cudaMalloc(&s.d_sig, 4 * sizeof(unsigned long long)));
+        CK(cudaMemset(s.d_sig, 0, 4 * sizeof(unsigned long long)));
+    }
+    return RTM_OK;
+}
+
+int export_record(rtm_ctx* c, IpcRecord* r) {
+    Slab& s = c->slabs[0];
+    RET(alloc_sig(s));
+    std::memset(r, 0, sizeof *r);
+    r->magic = kIpcMagic;
+    r->version = 1;
+    r->rank = c->rank;
+    r->world = c->world;
+    r->nx = c->nx;
+    r->ny = c->ny;
+    r->nz = c->nz;
+    r->nzl = s.nzl;
+    r->device = s.dev;
+    for (int b = 0; b < 2; ++b) CK(cudaIpcGetMemHandle(&r->buf[b], s.buf[b]));
+    CK(cudaIpcGetMemHandle(&r->sig, s.d_sig));
+    return RTM_OK;
+}
+
+int import_records(rtm_ctx* c, const IpcRecord* lo, const IpcRecord* hi) {
+    Slab& s = c->slabs[0];
+    if (c->ipc_imported) return fail(RTM_ESTATE, "the neighbours' IPC records are already imported");
+    if (s.lo_nb != (lo != nullptr) || s.hi_nb != (hi != nullptr))
+        return fail(RTM_EINVAL, "rank %d of %d needs %s lo record and %s hi record", c->rank, c->world,
+                    s.lo_nb ? "a" : "no", s.hi_nb ? "a" : "no");
+    for (int side = 0; side < 2; ++side) {
+        const IpcRecord* r = side == 0 ? lo : hi;
+        if (!r) continue;
+        const int want = c->rank + (side == 0 ? -1 : 1);
+        int z0, nzl;
+        if (r->magic != kIpcMagic || r->version != 1)
+            return fail(RTM_EINVAL, "%s record: not an RTM IPC record", side ? "hi" : "lo");
+        if (r->nx != c->nx || r->ny != c->ny || r->nz != c->nz || r->world != c->world || r->rank != want)
+            return fail(RTM_EINVAL, "%s record belongs to rank %d of %d on a %dx%dx%d grid (want rank %d of %d, %dx%dx%d)",
+                        side ? "hi" : "lo", r->rank, r->world, r->nx, r->ny, r->nz, want, c->world, c->nx, c->ny, c->nz);
+        RET(rtm_slab_range(c->nz, c->world, want, &z0, &nzl));
+        if (r->nzl != nzl) return fail(RTM_EINVAL, "%s record: nzl %d != %d", side ? "hi" : "lo", r->nzl, nzl);
+    }
+    CK(cudaSetDevice(s.dev));
+    RET(alloc_sig(s));
+    auto open = [&](const cudaIpcMemHandle_t& hd, void** out) -> int {
+        const cudaError_t e = cudaIpcOpenMemHandle(out, hd, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return fail(RTM_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+        s.ipc_open.push_back(*out);
+        return RTM_OK;
+    };
+    void* q;
+    if (lo) {
+        for (int b = 0; b < 2; ++b) {
+            RET(open(lo->buf[b], &q));
+            s.nb_lo[b] = static_cast<float*>(q);
+        }
+        RET(open(lo->sig, &q));
+        s.nb_lo_sig = static_cast<unsigned long long*>(q);
+        s.nb_lo_nzl = lo->nzl;
+    }
+    if (hi) {
+        for (int b = 0; b < 2; ++b) {
+            RET(open(hi->buf[b], &q));
+            s.nb_hi[b] = static_cast<float*>(q);
+        }
+        RET(open(hi->sig, &q));
+        s.nb_hi_sig = static_cast<unsigned long long*>(q);
+    }
+    // the neighbours' buffers follow the local time-level convention (u^n in buf[n & 1]): if a
+    // rtm_set_step_count swapped this rank's buffers, every rank swapped alike
+    c->ipc_imported = true;
+    return RTM_OK;
+}
+
+// Halo modes 2-3 set-up: flag words per slab, neighbours' buffer / flag pointers.  In-process
+// (mode 1) they are the other slabs' allocations; an NCCL-distributed context all-gathers the
+// IPC records over its communicator (a collective call); a peer context already imported them.
+// Ends with a rank barrier: no rank may signal into a neighbour's flag words before the
+// neighbour has cleared them.
 int setup_signal(rtm_ctx* c) {
     static PFN_devattr devattr = driver_fn<PFN_devattr>("cuDeviceGetAttribute");
     if (!devattr) return fail(RTM_ECUDA, "cuDeviceGetAttribute unavailable from the driver");
@@ -928,9 +1015,8 @@ int setup_signal(rtm_ctx* c) {
         devattr(&fl, CU_DEVICE_ATTRIBUTE_CAN_FLUSH_REMOTE_WRITES, (CUdevice)s.dev);
         if (!mem64) return fail(RTM_EINVAL, "device %d has no 64-bit stream memory operations", s.dev);
         if (!fl) flush = 0;
-        CK(cudaSetDevice(s.dev));
-        if (!s.d_sig) CK(cudaMalloc(&s.d_sig, 2 * sizeof(unsigned long long)));
-        CK(cudaMemset(s.d_sig, 0, 2 * sizeof(unsigned long long)));
+        RET(alloc_sig(s));
+        CK(cudaMemset(s.d_sig, 0, 4 * sizeof(unsigned long long)));
     }
     c->sig_flush = flush;
     const int G = (int)c->slabs.size();
@@ -946,14 +1032,11 @@ int setup_signal(rtm_ctx* c) {
                 s.nb_hi[0] = n.buf[0], s.nb_hi[1] = n.buf[1], s.nb_hi_sig = n.d_sig;
             }
         }
-    } else if (c->mode == 2) {
+    } else if (c->mode == 2 && !c->ipc_imported) {
         Slab& s = c->slabs[0];
         CK(cudaSetDevice(s.dev));
         IpcRecord mine;
-        std::memset(&mine, 0, sizeof mine);
-        for (int b = 0; b < 2; ++b) CK(cudaIpcGetMemHandle(&mine.buf[b], s.buf[b]));
-        CK(cudaIpcGetMemHandle(&mine.sig, s.d_sig));
-        mine.nzl = s.nzl;
+        RET(export_record(c, &mine));
         const int W = c->world;
         unsigned char* d = nullptr;
         CK(cudaMalloc(&d, (size_t)W * sizeof(IpcRecord)));
@@ -973,65 +1056,62 @@ int setup_signal(rtm_ctx* c) {
             rc = fail(RTM_ECUDA, "IPC record gather failed");
         cudaFree(d);
         RET(rc);
-        auto open = [&](const cudaIpcMemHandle_t& hd, void** out) -> int {
-            const cudaError_t e = cudaIpcOpenMemHandle(out, hd, cudaIpcMemLazyEnablePeerAccess);
-            if (e != cudaSuccess) return fail(RTM_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
-            s.ipc_open.push_back(*out);
-            return RTM_OK;
-        };
-        if (s.ipc_open.empty()) {
-            void* q;
-            if (s.lo_nb) {
-                const IpcRecord& n = all[c->rank - 1];
-                for (int b = 0; b < 2; ++b) {
-                    RET(open(n.buf[b], &q));
-                    s.nb_lo[b] = static_cast<float*>(q);
-                }
-                RET(open(n.sig, &q));
-                s.nb_lo_sig = static_cast<unsigned long long*>(q);
-                s.nb_lo_nzl = n.nzl;
-            }
-            if (s.hi_nb) {
-                const IpcRecord& n = all[c->rank + 1];
-                for (int b = 0; b < 2; ++b) {
-                    RET(open(n.buf[b], &q));
-                    s.nb_hi[b] = static_cast<float*>(q);
-                }
-                RET(open(n.sig, &q));
-                s.nb_hi_sig = static_cast<unsigned long long*>(q);
-            }
-        }
+        RET(import_records(c, s.lo_nb ? &all[c->rank - 1] : nullptr, s.hi_nb ? &all[c->rank + 1] : nullptr));
+    } else if (c->mode == 3 && c->world > 1 && !c->ipc_imported) {
+        return fail(RTM_ESTATE, "peer context: rtm_ipc_import the neighbours' records first");
     }
+    RET(ranks_barrier(c));
     ++c->sig_gen;
     c->sig_fresh = true;
     return RTM_OK;
 }
 
-// G > 1 step, fused halo push + flag protocol (f1, halo mode 2; across processes in mode 2):
-// step n on slab r waits (stream-side cuStreamWaitValue64, no spinning kernel) until both
-// neighbours have completed step n-1 — their pushes into r's halo have landed (RAW) and their
-// step n-1 reads of the halo planes r now overwrites are done (WAR) — then one stencil launch
-// whose epilogue also stores r's boundary planes into the neighbours' halos (peer / IPC
+typedef CUresult (*PFN_waitv64_t)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+PFN_waitv64_t waitv64() {
+    static PFN_waitv64_t f = driver_fn<PFN_waitv64_t>("cuStreamWaitValue64");
+    return f;
+}
+// Stream-side wait (no spinning kernel) until *flag >= v.
+int wait_flag(rtm_ctx* c, cudaStream_t st, unsigned long long* flag, unsigned long long v) {
+    auto f = waitv64();
+    if (!f) return fail(RTM_ECUDA, "cuStreamWaitValue64 unavailable from the driver");
+    const CUresult r = f((CUstream)st, (CUdeviceptr)flag, v, CU_STREAM_WAIT_VALUE_GEQ | c->sig_flush);
+    if (r != CUDA_SUCCESS) return fail(RTM_ECUDA, "cuStreamWaitValue64 failed (%d)", (int)r);
+    return RTM_OK;
+}
+
+// RTM_OPT_HOST_ORDERED: drain this context's streams, then meet every rank at the barrier —
+// after it, every flag a wait enqueued next targets has already been released.
+int host_order_point(rtm_ctx* c) {
+    if (!c->host_ordered) return RTM_OK;
+    for (auto& s : c->slabs) {
+        CK(cudaSetDevice(s.dev));
+        CK(cudaStreamSynchronize(s.stream()));
+        CK(cudaStreamSynchronize(s.s_comm));
+    }
+    return ranks_barrier(c);
+}
+
+// G > 1 step, fused halo push + flag protocol (f1, halo mode 2; across processes through the
+// IPC mappings): step n on slab r waits (stream-side cuStreamWaitValue64, no spinning kernel)
+// until both neighbours have completed step n-1 — their pushes into r's halo have landed (RAW)
+// and their step n-1 reads of the halo planes r now overwrites are done (WAR) — then one stencil
+// launch whose epilogue also stores r's boundary planes into the neighbours' halos (peer / IPC
 // stores over NVLink), then k_signal releases "steps done = n+1" into the neighbours' flags.
 // Values carry a generation (bumped by every synchronising reset), so stale flags never pass.
 int step_slabs_signal(rtm_ctx* c, int nsteps) {
-    static PFN_waitv64 waitv = driver_fn<PFN_waitv64>("cuStreamWaitValue64");
-    if (!waitv) return fail(RTM_ECUDA, "cuStreamWaitValue64 unavailable from the driver");
     const size_t plane = dplane(c);
     const unsigned long long g = c->sig_gen << 40;
     for (int k = 0; k < nsteps; ++k) {
         const int parity = (int)(c->step & 1);
         const unsigned long long n = (unsigned long long)c->step;
+        RET(host_order_point(c));
         for (auto& s : c->slabs) {
             CK(cudaSetDevice(s.dev));
             cudaStream_t st = s.stream();
             if (!c->sig_fresh) {
-                for (int side = 0; side < 2; ++side)
-                    if (side == 0 ? s.lo_nb : s.hi_nb) {
-                        const CUresult r = waitv((CUstream)st, (CUdeviceptr)(s.d_sig + side), g | n,
-                                                 CU_STREAM_WAIT_VALUE_GEQ | c->sig_flush);
-                        if (r != CUDA_SUCCESS) return fail(RTM_ECUDA, "cuStreamWaitValue64 failed (%d)", (int)r);
-                    }
+                if (s.lo_nb) RET(wait_flag(c, st, s.d_sig + 0, g | n));
+                if (s.hi_nb) RET(wait_flag(c, st, s.d_sig + 1, g | n));
             }
             float* lo = s.lo_nb ? s.nb_lo[parity ^ 1] + (size_t)(s.nb_lo_nzl + 5) * plane : nullptr;
             float* hi = s.hi_nb ? s.nb_hi[parity ^ 1] : nullptr;
@@ -1045,58 +1125,290 @@ int step_slabs_signal(rtm_ctx* c, int nsteps) {
     return RTM_OK;
 }
 
-// G > 1 step: boundary planes first, exchange on the comm stream, interior concurrently.
-int step_slabs(rtm_ctx* c, int nsteps) {
-    if (c->mode == 1 && c->halo_mode == 1) return step_slabs_fused(c, nsteps);
-    if (c->halo_mode == 2) return step_slabs_signal(c, nsteps);
-    const int G = (int)c->slabs.size();
+// G > 1 step, copy-engine pull + flag protocol (halo mode 3; SURVEY §8(e) "SM-free
+// alternative"; in-process or across processes through the IPC mappings).  Step n on slab r:
+//   stream:  boundary planes [0,5) + [nzl-5,nzl) of u^{n+1} (after r's own pulls of step n-1:
+//            stream order), then k_signal B := g|(n+1) into the neighbours ("boundary of step
+//            n ready");
+//   comm:    after the boundary (event), wait B_lo, B_hi >= g|(n+1) [RAW], then cudaMemcpyAsync
+//            the neighbours' 5 boundary planes of u^{n+1} into r's own halo planes (copy engines
+//            reading the peer / IPC mapping; no SM time, no NCCL kernels);
+//   stream:  interior planes [5, nzl-5) (overlapping the pulls), then wait for the pulls (event).
+// Every rank writes only its own memory.  The WAR hazard — r's boundary of step n overwrites the
+// u^{n-1} planes a neighbour pulled at its step n-2 — needs no flag of its own: r's boundary n
+// follows r's pulls of n-1, which waited for the neighbour's boundary n-1, which followed the
+// neighbour's pulls of n-2 (model-checked in tests/test_halo_protocol_model.py).
+int step_slabs_pull(rtm_ctx* c, int nsteps) {
+    const size_t plane = dplane(c);
+    const size_t bytes = 5 * plane * sizeof(float);
+    const unsigned long long g = c->sig_gen << 40;
     for (int k = 0; k < nsteps; ++k) {
         const int parity = (int)(c->step & 1);
-        for (int r = 0; r < G; ++r) {
-            Slab& s = c->slabs[r];
+        const unsigned long long n = (unsigned long long)c->step;
+        for (auto& s : c->slabs) {
             CK(cudaSetDevice(s.dev));
-            for (int d = -1; d <= 1; ++d)  // previous exchange done (reads and writes)
-                if (r + d >= 0 && r + d < G) CK(cudaStreamWaitEvent(s.stream(), c->slabs[r + d].ev_comm, 0));
+            cudaStream_t st = s.stream();
             if (s.lo_nb || s.hi_nb) {
                 const int b0 = s.lo_nb ? 0 : s.nzl - 5;
-                const int l0 = 5;
                 const int b1 = s.nzl - 5, l1 = (s.lo_nb && s.hi_nb) ? 5 : 0;
-                RET(launch_stencil(c, s, parity, b0, l0, b1, l1, 0, s.stream()));
+                RET(launch_stencil(c, s, parity, b0, 5, b1, l1, 0, st));
+                CK(launch_signal(s.lo_nb ? s.nb_lo_sig + 3 : nullptr, s.hi_nb ? s.nb_hi_sig + 2 : nullptr,
+                                 g | (n + 1), st));
             }
-            CK(cudaEventRecord(s.ev_bnd, s.stream()));
+            CK(cudaEventRecord(s.ev_bnd, st));
         }
-        if (c->mode == 2) RET(exchange_nccl(c, parity ^ 1));
-        else RET(exchange_local(c, parity ^ 1));
-        for (int r = 0; r < G; ++r) {
-            Slab& s = c->slabs[r];
+        RET(host_order_point(c));
+        for (auto& s : c->slabs) {
             CK(cudaSetDevice(s.dev));
+            cudaStream_t st = s.stream();
+            float* dst = s.buf[parity ^ 1];
+            if (s.lo_nb || s.hi_nb) {
+                CK(cudaStreamWaitEvent(s.s_comm, s.ev_bnd, 0));
+                if (s.lo_nb) {
+                    RET(wait_flag(c, s.s_comm, s.d_sig + 2, g | (n + 1)));
+                    CK(cudaMemcpyAsync(dst, s.nb_lo[parity ^ 1] + (size_t)s.nb_lo_nzl * plane, bytes,
+                                       cudaMemcpyDefault, s.s_comm));
+                }
+                if (s.hi_nb) {
+                    RET(wait_flag(c, s.s_comm, s.d_sig + 3, g | (n + 1)));
+                    CK(cudaMemcpyAsync(dst + (size_t)(s.nzl + 5) * plane, s.nb_hi[parity ^ 1] + 5 * plane,
+                                       bytes, cudaMemcpyDefault, s.s_comm));
+                }
+                CK(cudaEventRecord(s.ev_comm, s.s_comm));
+            }
             const int ib = s.lo_nb ? 5 : 0;
             const int ie = s.hi_nb ? s.nzl - 5 : s.nzl;
-            RET(launch_stencil(c, s, parity, ib, ie - ib, 0, 0, 1, s.stream()));
+            RET(launch_stencil(c, s, parity, ib, ie - ib, 0, 0, 1, st));
+            if (s.lo_nb || s.hi_nb) CK(cudaStreamWaitEvent(st, s.ev_comm, 0));
         }
+        c->sig_fresh = false;
         ++c->step;
-    }
-    for (int r = 0; r < G; ++r) {  // join: the field is complete when the step returns
-        Slab& s = c->slabs[r];
-        CK(cudaSetDevice(s.dev));
-        for (int d = -1; d <= 1; ++d)
-            if (r + d >= 0 && r + d < G) CK(cudaStreamWaitEvent(s.stream(), c->slabs[r + d].ev_comm, 0));
     }
     return RTM_OK;
 }
 
-// Barrier across the ranks of a distributed context (NCCL all-reduce of one value, then a
-// stream synchronisation): on return every rank has reached this call.
-int comm_barrier(rtm_ctx* c) {
-    Slab& s = c->slabs[0];
-    CK(cudaSetDevice(s.dev));
-    double* d = nullptr;
-    CK(cudaMalloc(&d, sizeof(double)));
-    const ncclResult_t nr = ncclAllReduce(d, d, 1, ncclFloat64, ncclSum, c->comm, s.stream());
-    const cudaError_t e = cudaStreamSynchronize(s.stream());
-    cudaFree(d);
-    if (nr != ncclSuccess || e != cudaSuccess) return fail(RTM_ENCCL, "rank barrier failed");
+// Halo fill of u^{parity} from the neighbours' owned planes through the peer / IPC mappings
+// (peer contexts' rtm_reset / rtm_set_fields; synchronous, after a rank barrier).
+int pull_halos_now(rtm_ctx* c, int parity) {
+    const size_t plane = dplane(c);
+    const size_t bytes = 5 * plane * sizeof(float);
+    RET(ranks_barrier(c));  // every rank's initial data is in place
+    for (auto& s : c->slabs) {
+        CK(cudaSetDevice(s.dev));
+        float* dst = s.buf[parity];
+        if (s.lo_nb)
+            CK(cudaMemcpyAsync(dst, s.nb_lo[parity] + (size_t)s.nb_lo_nzl * plane, bytes, cudaMemcpyDefault, s.s_comm));
+        if (s.hi_nb)
+            CK(cudaMemcpyAsync(dst + (size_t)(s.nzl + 5) * plane, s.nb_hi[parity] + 5 * plane, bytes,
+                               cudaMemcpyDefault, s.s_comm));
+        CK(cudaStreamSynchronize(s.s_comm));
+    }
     return RTM_OK;
+}
+
+// One G > 1 step with boundary planes first, the exchange on the comm streams (NCCL or
+// in-process copy engines), interior concurrently (halo mode 0).
+int enqueue_slab_step0(rtm_ctx* c) {
+    const int G = (int)c->slabs.size();
+    const int parity = (int)(c->step & 1);
+    for (int r = 0; r < G; ++r) {
+        Slab& s = c->slabs[r];
+        CK(cudaSetDevice(s.dev));
+        for (int d = -1; d <= 1; ++d)  // previous exchange done (reads and writes)
+            if (r + d >= 0 && r + d < G) CK(cudaStreamWaitEvent(s.stream(), c->slabs[r + d].ev_comm, 0));
+        if (s.lo_nb || s.hi_nb) {
+            const int b0 = s.lo_nb ? 0 : s.nzl - 5;
+            const int l0 = 5;
+            const int b1 = s.nzl - 5, l1 = (s.lo_nb && s.hi_nb) ? 5 : 0;
+            RET(launch_stencil(c, s, parity, b0, l0, b1, l1, 0, s.stream()));
+        }
+        CK(cudaEventRecord(s.ev_bnd, s.stream()));
+    }
+    if (c->mode == 2) RET(exchange_nccl(c, parity ^ 1));
+    else RET(exchange_local(c, parity ^ 1));
+    for (int r = 0; r < G; ++r) {
+        Slab& s = c->slabs[r];
+        CK(cudaSetDevice(s.dev));
+        const int ib = s.lo_nb ? 5 : 0;
+        const int ie = s.hi_nb ? s.nzl - 5 : s.nzl;
+        RET(launch_stencil(c, s, parity, ib, ie - ib, 0, 0, 1, s.stream()));
+    }
+    ++c->step;
+    return RTM_OK;
+}
+
+// One G > 1 step of the event-ordered fused push (in-process halo mode 1): one launch per
+// slab whose epilogue also stores the boundary planes into the neighbours' z-halo.  Step n on
+// slab r waits for step n-1 of r-1, r, r+1: their pushes into r's halo (RAW) and their reads of
+// the halo planes r is about to overwrite (WAR).
+int enqueue_slab_step1(rtm_ctx* c) {
+    const int G = (int)c->slabs.size();
+    const size_t plane = dplane(c);
+    const int parity = (int)(c->step & 1);
+    for (int r = 0; r < G; ++r) {
+        Slab& s = c->slabs[r];
+        CK(cudaSetDevice(s.dev));
+        for (int d = -1; d <= 1; d += 2)
+            if (r + d >= 0 && r + d < G) CK(cudaStreamWaitEvent(s.stream(), c->slabs[r + d].ev_done, 0));
+    }
+    for (int r = 0; r < G; ++r) {
+        Slab& s = c->slabs[r];
+        CK(cudaSetDevice(s.dev));
+        float* lo = s.lo_nb ? c->slabs[r - 1].buf[parity ^ 1] + (size_t)(c->slabs[r - 1].nzl + 5) * plane
+                            : nullptr;
+        float* hi = s.hi_nb ? c->slabs[r + 1].buf[parity ^ 1] : nullptr;
+        RET(launch_stencil(c, s, parity, 0, s.nzl, 0, 0, 1, s.stream(), lo, hi));
+        CK(cudaEventRecord(s.ev_done, s.stream()));
+    }
+    ++c->step;
+    return RTM_OK;
+}
+
+// Join: every slab's stream waits for its neighbours' last exchange / push events, so the
+// field is complete when rtm_step's final synchronisation returns.
+int join_slabs(rtm_ctx* c) {
+    const int G = (int)c->slabs.size();
+    for (int r = 0; r < G; ++r) {
+        Slab& s = c->slabs[r];
+        CK(cudaSetDevice(s.dev));
+        for (int d = -1; d <= 1; ++d)
+            if (r + d >= 0 && r + d < G) {
+                CK(cudaStreamWaitEvent(s.stream(), c->slabs[r + d].ev_comm, 0));
+                CK(cudaStreamWaitEvent(s.stream(), c->slabs[r + d].ev_done, 0));
+            }
+    }
+    return RTM_OK;
+}
+
+// CUDA graph of 2*GRAPH_PAIRS event-ordered slab steps (halo modes 0 and 1, in-process or NCCL):
+// captured from slab 0's stream, the other slabs' streams (and comm streams) join the capture
+// through an event and are joined back at the end, so one cudaGraphLaunch replays every
+// slab's launches, copies / NCCL calls and event edges.  Starts at an even step (parity 0);
+// every captured parameter (buffers, ranges, step-counter slots) repeats with period 2.
+int build_slab_graph(rtm_ctx* c) {
+    Slab& s0 = c->slabs[0];
+    const int var = single_variant(c);
+    if (s0.graph_valid && s0.graph_variant == var) return RTM_OK;
+    if (s0.graph) cudaGraphExecDestroy(s0.graph), s0.graph = nullptr;
+    if (s0.graph_def) cudaGraphDestroy(s0.graph_def), s0.graph_def = nullptr;
+    for (auto& s : c->slabs) RET(ensure_tmaps(c, s, var));
+    CK(cudaSetDevice(s0.dev));
+    cudaStream_t origin = s0.stream();
+    CK(cudaStreamBeginCapture(origin, cudaStreamCaptureModeRelaxed));
+    const long long saved_step = c->step, saved_launches = c->launches;
+    int rc = RTM_OK;
+    cudaEvent_t fork = nullptr;
+    if (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) rc = fail(RTM_ECUDA, "event");
+    if (rc == RTM_OK && cudaEventRecord(fork, origin) != cudaSuccess) rc = fail(RTM_ECUDA, "fork record");
+    for (auto& s : c->slabs) {  // every stream of the step joins the capture
+        if (rc != RTM_OK) break;
+        cudaSetDevice(s.dev);
+        if ((&s != &s0 && cudaStreamWaitEvent(s.stream(), fork, 0) != cudaSuccess) ||
+            cudaStreamWaitEvent(s.s_comm, fork, 0) != cudaSuccess)
+            rc = fail(RTM_ECUDA, "capture fork failed");
+        // the events of the previous step are outside the capture: re-record them inside
+        if (rc == RTM_OK && (cudaEventRecord(s.ev_comm, s.s_comm) != cudaSuccess ||
+                             cudaEventRecord(s.ev_done, s.stream()) != cudaSuccess))
+            rc = fail(RTM_ECUDA, "capture event re-record failed");
+    }
+    c->step = 0;
+    for (int k = 0; k < 2 * GRAPH_PAIRS && rc == RTM_OK; ++k)
+        rc = c->halo_mode == 1 ? enqueue_slab_step1(c) : enqueue_slab_step0(c);
+    if (rc == RTM_OK) rc = join_slabs(c);
+    for (auto& s : c->slabs) {  // join every stream back into the origin
+        if (rc != RTM_OK) break;
+        cudaSetDevice(s.dev);
+        if (cudaEventRecord(s.ev_bnd, s.s_comm) != cudaSuccess) rc = fail(RTM_ECUDA, "join record");
+        cudaSetDevice(s0.dev);
+        if (rc == RTM_OK && cudaStreamWaitEvent(origin, s.ev_bnd, 0) != cudaSuccess) rc = fail(RTM_ECUDA, "join");
+        if (&s != &s0 && rc == RTM_OK) {
+            cudaSetDevice(s.dev);
+            if (cudaEventRecord(s.ev_bnd, s.stream()) != cudaSuccess) rc = fail(RTM_ECUDA, "join record");
+            cudaSetDevice(s0.dev);
+            if (rc == RTM_OK && cudaStreamWaitEvent(origin, s.ev_bnd, 0) != cudaSuccess) rc = fail(RTM_ECUDA, "join");
+        }
+    }
+    cudaSetDevice(s0.dev);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(origin, &g);
+    c->step = saved_step;
+    c->launches = saved_launches;
+    if (fork) cudaEventDestroy(fork);
+    if (rc == RTM_OK && e != cudaSuccess) rc = fail(RTM_ECUDA, "slab graph capture failed: %s", cudaGetErrorString(e));
+    if (rc != RTM_OK) {
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        return rc;
+    }
+    s0.graph_def = g;
+    if (cudaGraphInstantiate(&s0.graph, g, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(RTM_ECUDA, "slab graph instantiate failed");
+    }
+    s0.graph_valid = true;
+    s0.graph_variant = var;
+    return RTM_OK;
+}
+
+// G > 1 steps (halo modes 0-3).
+int step_slabs(rtm_ctx* c, int nsteps) {
+    if (c->halo_mode == 2) return step_slabs_signal(c, nsteps);
+    if (c->halo_mode == 3) return step_slabs_pull(c, nsteps);
+    long long launches_per_step = 0;
+    for (auto& s : c->slabs) launches_per_step += (c->halo_mode == 0 && (s.lo_nb || s.hi_nb)) ? 2 : 1;
+    int k = 0;
+    while (k < nsteps) {
+        const bool even = (c->step & 1) == 0;
+        if (c->graphs && !c->profiling && !c->slab_graphs_broken && even && nsteps - k >= 2 * GRAPH_PAIRS) {
+            if (build_slab_graph(c) != RTM_OK) {
+                // e.g. a capture the driver refuses: direct launches from now on.  Events last
+                // recorded inside the aborted capture cannot be waited on: re-record them.
+                if (std::getenv("RTM_DEBUG")) std::fprintf(stderr, "rtm: slab graph capture failed: %s\n", g_err.c_str());
+                c->slab_graphs_broken = true;
+                g_err.clear();
+                cudaGetLastError();
+                for (auto& s : c->slabs) {
+                    CK(cudaSetDevice(s.dev));
+                    CK(cudaEventRecord(s.ev_comm, s.s_comm));
+                    CK(cudaEventRecord(s.ev_done, s.stream()));
+                    CK(cudaEventRecord(s.ev_bnd, s.stream()));
+                }
+                continue;
+            }
+            Slab& s0 = c->slabs[0];
+            // the graph runs on slab 0's stream: it starts after every stream's pending work
+            // and every stream's later work starts after it
+            for (auto& s : c->slabs) {
+                CK(cudaSetDevice(s.dev));
+                CK(cudaEventRecord(s.ev_bnd, s.s_comm));
+                CK(cudaSetDevice(s0.dev));
+                CK(cudaStreamWaitEvent(s0.stream(), s.ev_bnd, 0));
+                if (&s != &s0) {
+                    CK(cudaSetDevice(s.dev));
+                    CK(cudaEventRecord(s.ev_bnd, s.stream()));
+                    CK(cudaSetDevice(s0.dev));
+                    CK(cudaStreamWaitEvent(s0.stream(), s.ev_bnd, 0));
+                }
+            }
+            CK(cudaSetDevice(s0.dev));
+            CK(cudaGraphLaunch(s0.graph, s0.stream()));
+            CK(cudaEventRecord(s0.ev_bnd, s0.stream()));
+            for (auto& s : c->slabs) {
+                CK(cudaSetDevice(s.dev));
+                CK(cudaStreamWaitEvent(s.s_comm, s0.ev_bnd, 0));
+                if (&s != &s0) CK(cudaStreamWaitEvent(s.stream(), s0.ev_bnd, 0));
+                CK(cudaEventRecord(s.ev_comm, s.s_comm));  // the neighbours' next waits see the graph
+                CK(cudaEventRecord(s.ev_done, s.stream()));
+            }
+            c->step += 2 * GRAPH_PAIRS;
+            c->launches += launches_per_step * 2 * GRAPH_PAIRS;
+            k += 2 * GRAPH_PAIRS;
+            continue;
+        }
+        RET(c->halo_mode == 1 ? enqueue_slab_step1(c) : enqueue_slab_step0(c));
+        ++k;
+    }
+    return join_slabs(c);
 }
 
 int sync_all(rtm_ctx* c) {
@@ -1204,6 +1516,11 @@ int reset_impl(rtm_ctx* c, const float* u, const float* up) {
     // only remote write into this slab's buf[1] halo planes is then the neighbour's push, and
     // the neighbour can only push after this exchange, i.e. after this rank's reset memsets
     // (stream order on the sending side of the exchange).
+    if (c->mode == 3) {  // peer context: pull through the IPC mappings after a barrier
+        RET(sync_all(c));
+        if (c->world > 1) RET(pull_halos_now(c, 0));
+        return RTM_OK;
+    }
     if (c->slabs.size() > 1 || c->mode == 2) {
         for (auto& s : c->slabs) {
             CK(cudaSetDevice(s.dev));
@@ -1476,6 +1793,68 @@ rtm_ctx* rtm_create_dist(int nx, int ny, int nz_global, float dx, float dt,
     return c;
 }
 
+rtm_ctx* rtm_create_peer(int nx, int ny, int nz_global, float dx, float dt, const float coeffs[6],
+                         int rank, int world, int device) {
+    DeviceGuard g;
+    int z0, nzl;
+    if (rtm_slab_range(nz_global, world, rank, &z0, &nzl) != RTM_OK) return nullptr;
+    int ndev = 0;
+    cudaGetDeviceCount(&ndev);
+    if (device < 0 || device >= ndev) {
+        fail(RTM_EINVAL, "device %d is not a CUDA device (count %d)", device, ndev);
+        return nullptr;
+    }
+    rtm_ctx* c = new_ctx(nx, ny, nz_global, dx, dt, coeffs);
+    if (!c) return nullptr;
+    c->mode = 3;
+    c->rank = rank;
+    c->world = world;
+    c->halo_mode = 3;
+    Slab s;
+    s.dev = device;
+    s.z0 = z0;
+    s.nzl = nzl;
+    s.lo_nb = rank > 0;
+    s.hi_nb = rank < world - 1;
+    c->slabs.push_back(s);
+    if (finish_ctx(c) != RTM_OK || alloc_sig(c->slabs[0]) != RTM_OK) {
+        std::string e = g_err;
+        destroy_ctx(c);
+        g_err = e;
+        return nullptr;
+    }
+    return c;
+}
+
+int rtm_ipc_export(rtm_ctx* c, unsigned char rec[RTM_IPC_RECORD_BYTES]) {
+    if (!c || !rec) return fail(RTM_EINVAL, "NULL argument");
+    if (c->mode != 2 && c->mode != 3) return fail(RTM_EINVAL, "IPC records belong to distributed or peer contexts");
+    DeviceGuard g;
+    IpcRecord r;
+    RET(export_record(c, &r));
+    std::memcpy(rec, &r, sizeof r);
+    return RTM_OK;
+}
+
+int rtm_ipc_import(rtm_ctx* c, const unsigned char* lo, const unsigned char* hi) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    if (c->mode != 2 && c->mode != 3) return fail(RTM_EINVAL, "IPC records belong to distributed or peer contexts");
+    DeviceGuard g;
+    IpcRecord rl, rh;
+    if (lo) std::memcpy(&rl, lo, sizeof rl);
+    if (hi) std::memcpy(&rh, hi, sizeof rh);
+    return import_records(c, lo ? &rl : nullptr, hi ? &rh : nullptr);
+}
+
+int rtm_set_host_barrier(rtm_ctx* c, rtm_barrier_fn fn, void* user) {
+    if (!c) return fail(RTM_EINVAL, "ctx is NULL");
+    c->barrier_fn = fn;
+    c->barrier_user = user;
+    return RTM_OK;
+}
+
+double rtm_last_enqueue_ms(rtm_ctx* c) { return c ? c->enqueue_ms : -1.0; }
+
 void rtm_destroy(rtm_ctx* ctx) { destroy_ctx(ctx); }
 
 int rtm_set_velocity(rtm_ctx* c, const float* v) {
@@ -1558,6 +1937,9 @@ int rtm_step(rtm_ctx* c, int nsteps) {
         }
         return RTM_OK;
     }
+    if (c->mode == 3 && c->world > 1 && !c->ipc_imported)
+        return fail(RTM_ESTATE, "peer context: rtm_ipc_import the neighbours' records before rtm_step");
+    const auto h0 = std::chrono::steady_clock::now();
     CK(cudaEventRecord(c->t0, s0.stream()));
     if (c->mode == 0) {
         RET(step_single(c, nsteps));
@@ -1575,6 +1957,7 @@ int rtm_step(rtm_ctx* c, int nsteps) {
     }
     CK(cudaSetDevice(s0.dev));
     CK(cudaEventRecord(c->t1, s0.stream()));
+    c->enqueue_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
     RET(sync_all(c));
     CK(cudaEventElapsedTime(&c->last_ms, c->t0, c->t1));
     RET(collect_profile(c));
@@ -1637,7 +2020,7 @@ int rtm_get_dims(rtm_ctx* c, int* nx, int* ny, int* nzl, int* nshots) {
     if (!c) return fail(RTM_EINVAL, "ctx is NULL");
     if (nx) *nx = c->nx;
     if (ny) *ny = c->ny;
-    if (nzl) *nzl = c->mode == 2 ? c->slabs[0].nzl : c->nz;
+    if (nzl) *nzl = (c->mode == 2 || c->mode == 3) ? c->slabs[0].nzl : c->nz;
     if (nshots) *nshots = c->slabs[0].nshots;
     return RTM_OK;
 }
@@ -1664,8 +2047,8 @@ int rtm_set_step_count(rtm_ctx* c, long long n) {
         CK(cudaMemcpy(s.d_step, h, sizeof h, cudaMemcpyHostToDevice));
     }
     c->step = n;
-    if (c->halo_mode == 2) {  // flags restart: make the call collective across ranks
-        if (c->comm) RET(comm_barrier(c));
+    if (c->halo_mode >= 2) {  // flags restart: make the call collective across ranks
+        RET(ranks_barrier(c));
         ++c->sig_gen;
         c->sig_fresh = true;
     }
@@ -1744,12 +2127,18 @@ int rtm_set_option(rtm_ctx* c, int key, long long value) {
             if (value < 0 || value > 1) return fail(RTM_EINVAL, "pdl %lld not in 0..1", value);
             c->pdl = value != 0;
             break;
+        case RTM_OPT_HOST_ORDERED:
+            if (value < 0 || value > 1) return fail(RTM_EINVAL, "host ordered %lld not in 0..1", value);
+            c->host_ordered = value != 0;
+            break;
         case RTM_OPT_HALO_MODE:
-            if (value < 0 || value > 2) return fail(RTM_EINVAL, "halo mode %lld not in 0..2", value);
+            if (value < 0 || value > 3) return fail(RTM_EINVAL, "halo mode %lld not in 0..3", value);
+            if (value == 0 && c->mode == 3 && c->world > 1)
+                return fail(RTM_EINVAL, "halo mode 0 (NCCL / in-process copies) is not available in a peer context (no NCCL)");
             if (value == 1 && c->mode != 1)
                 return fail(RTM_EINVAL, "halo mode 1 (fused push, event ordered) needs an in-process multi-slab context");
-            if (value == 2 && c->mode == 0)
-                return fail(RTM_EINVAL, "halo mode 2 (fused push, flag protocol) needs a multi-slab or distributed context");
+            if (value >= 2 && c->mode == 0)
+                return fail(RTM_EINVAL, "halo modes 2-3 (flag protocol) need a multi-slab, distributed or peer context");
             if (value >= 1 && c->mode == 1) {  // every slab must be able to store into its neighbours
                 for (size_t r = 0; r + 1 < c->slabs.size(); ++r) {
                     const int a = c->slabs[r].dev, b = c->slabs[r + 1].dev;
@@ -1765,7 +2154,7 @@ int rtm_set_option(rtm_ctx* c, int key, long long value) {
             {  // switch cleanly: drain first (mode 2 contexts: a collective call)
                 DeviceGuard g;
                 RET(sync_all(c));
-                if (value == 2) RET(setup_signal(c));
+                if (value >= 2) RET(setup_signal(c));
                 c->halo_mode = (int)value;
             }
             break;
@@ -1787,6 +2176,7 @@ long long rtm_get_option(rtm_ctx* c, int key) {
         case RTM_OPT_CHECK_EVERY: return c->check_every;
         case RTM_OPT_TB_CTAS: return c->tb_ctas;
         case RTM_OPT_PDL: return c->pdl ? 1 : 0;
+        case RTM_OPT_HOST_ORDERED: return c->host_ordered ? 1 : 0;
         default: return -1;
     }
 }
@@ -1922,7 +2312,10 @@ int rtm_autotune(rtm_ctx* c, int nI, const int* tiles, const int* zchunks, int n
         invalidate_graphs(c);
         rc = timed_steps(c, nI, &actual, d_scratch);
     }
-    // restore the wavefield and step counter (always, even on failure)
+    // restore the wavefield and step counter (always, even on failure).  A peer context has
+    // no all-reduce in the timed phases: meet at the barrier first, so no neighbour is still
+    // stepping (pushing into / pulling from this slab) while it is restored.
+    if (!c->comm && c->mode == 3 && rc == RTM_OK) rc = ranks_barrier(c);
     for (size_t k = 0; k < c->slabs.size(); ++k) {
         Slab& s = c->slabs[k];
         cudaSetDevice(s.dev);
@@ -1935,13 +2328,13 @@ int rtm_autotune(rtm_ctx* c, int nI, const int* tiles, const int* zchunks, int n
     }
     c->step = saved_step;
     cleanup();
-    if (c->halo_mode == 2) {
+    if (c->halo_mode >= 2) {
         // The flag words hold g|(steps reached while tuning), beyond every later target g|n:
         // start a new generation so the waits order the slabs again.  Across ranks the restore
         // must also be complete everywhere before anyone pushes into a neighbour's halo: the
         // timed phases end in an all-reduce (all ranks' tuning steps done), and this barrier
         // orders every rank's restore before the next step of any rank.
-        if (c->comm && rc == RTM_OK) rc = comm_barrier(c);
+        if (rc == RTM_OK) rc = ranks_barrier(c);
         ++c->sig_gen;
         c->sig_fresh = true;
     }

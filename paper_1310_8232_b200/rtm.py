@@ -22,6 +22,8 @@ RTM_OPT_ZCHUNK, RTM_OPT_CACHE_MODE, RTM_OPT_GRAPHS, RTM_OPT_SHOT_ORDER, RTM_OPT_
 RTM_OPT_CHECK_EVERY = 6
 RTM_OPT_TB_CTAS = 7
 RTM_OPT_PDL = 8
+RTM_OPT_HOST_ORDERED = 9
+RTM_IPC_RECORD_BYTES = 512
 _NAMES = {0: "RTM_OK", -1: "RTM_EINVAL", -2: "RTM_ECFL", -3: "RTM_ENOMEM", -4: "RTM_ECUDA",
           -5: "RTM_ENCCL", -6: "RTM_ESTATE", -7: "RTM_EUNSTABLE"}
 
@@ -90,7 +92,14 @@ _SIGS = {
     "rtm_step_async": (_I, [_P, _I]),
     "rtm_read_field_async": (_I, [_P, _P]),
     "rtm_sync": (_I, [_P]),
+    "rtm_create_peer": (_P, [_I, _I, _I, _F, _F, _P, _I, _I, _I]),
+    "rtm_ipc_export": (_I, [_P, _P]),
+    "rtm_ipc_import": (_I, [_P, _P, _P]),
+    "rtm_set_host_barrier": (_I, [_P, _P, _P]),
+    "rtm_last_enqueue_ms": (_D, [_P]),
 }
+BARRIER_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)
+_barriers: dict = {}  # handle -> the ctypes callback object (kept alive while installed)
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)
     _f.restype = _res
@@ -188,6 +197,7 @@ def rtm_read_field(h, out):
 def rtm_destroy(h):
     if h:
         lib.rtm_destroy(h)
+        _barriers.pop(h, None)
 
 
 def rtm_last_error() -> str:
@@ -412,3 +422,54 @@ def rtm_select_mwmb(times) -> int:
     if t.ndim != 2:
         raise ValueError("times must be (nranks, ncand)")
     return int(lib.rtm_select_mwmb(_ptr(t), int(t.shape[0]), int(t.shape[1])))
+
+
+# ---- peer contexts: CUDA-IPC data plane without NCCL -----------------------------------
+def rtm_create_peer(nx, ny, nz_global, dx, dt, coeffs, rank, world, device):
+    c = _coeffs(coeffs)
+    h = lib.rtm_create_peer(int(nx), int(ny), int(nz_global), float(dx), float(dt), _ptr(c),
+                            int(rank), int(world), int(device))
+    if not h:
+        raise RtmError(RTM_ECUDA if "CUDA" in _err() else RTM_EINVAL, _err())
+    return h
+
+
+def rtm_ipc_export(h) -> bytes:
+    buf = (ctypes.c_ubyte * RTM_IPC_RECORD_BYTES)()
+    _check(lib.rtm_ipc_export(h, ctypes.cast(buf, _P)))
+    return bytes(buf)
+
+
+def rtm_ipc_import(h, lo: bytes | None, hi: bytes | None):
+    def arg(r, name):
+        if r is None:
+            return None, None
+        if len(r) != RTM_IPC_RECORD_BYTES:
+            raise ValueError(f"{name} record must be {RTM_IPC_RECORD_BYTES} bytes")
+        b = (ctypes.c_ubyte * RTM_IPC_RECORD_BYTES).from_buffer_copy(r)
+        return b, ctypes.cast(b, _P)
+    bl, pl = arg(lo, "lo")
+    bh, ph = arg(hi, "hi")
+    return _check(lib.rtm_ipc_import(h, pl, ph))
+
+
+def rtm_set_host_barrier(h, fn):
+    """fn() -> None: returns once every rank called it (e.g. a gloo-group barrier); an
+    exception inside it makes the calling library operation fail with RTM_ESTATE."""
+    if fn is None:
+        _barriers.pop(h, None)
+        return _check(lib.rtm_set_host_barrier(h, None, None))
+
+    def tramp(_user):
+        try:
+            fn()
+            return 0
+        except Exception:  # noqa: BLE001  (reported to the caller as RTM_ESTATE)
+            return 1
+    cb = BARRIER_FN(tramp)
+    _barriers[h] = cb
+    return _check(lib.rtm_set_host_barrier(h, ctypes.cast(cb, _P), None))
+
+
+def rtm_last_enqueue_ms(h) -> float:
+    return float(lib.rtm_last_enqueue_ms(h))

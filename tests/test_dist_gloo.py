@@ -106,3 +106,37 @@ def test_gloo_slabs_equal_unsplit_oracle(world):
     status, equal, err = q.get(timeout=10)
     assert status == "ok", equal
     assert equal, err
+
+
+def _rec_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1310_8232_b200 import dist as pd
+        rec = bytes([rank]) * 512  # stands in for rtm_ipc_export's 512-byte record
+        lo, hi = pd.exchange_neighbour_records(rec, rank, world)
+        q.put((rank, None if lo is None else lo[0], None if hi is None else hi[0],
+               None if lo is None else len(lo)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_ipc_record_exchange_gives_each_rank_its_neighbours(world):
+    """The peer-context bootstrap (paper_1310_8232_b200.dist): every rank receives exactly the
+    records of rank-1 and rank+1 (None at the ends), unmodified."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rec_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    assert all(p.exitcode == 0 for p in procs)
+    got = sorted(q.get(timeout=10) for _ in range(world))
+    for rank, lo, hi, n in got:
+        assert lo == (rank - 1 if rank > 0 else None)
+        assert hi == (rank + 1 if rank < world - 1 else None)
+        assert n in (None, 512)

@@ -4,10 +4,14 @@ the binding.  Each compares against the G = 1 single-step kernel bitwise (R14, S
 P11) or checks an error contract of include/rtm.h."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
 import rtm_inputs as ri
+
+os.environ.setdefault("RTM_DEBUG", "1")  # the library reports a refused graph capture on stderr
 
 pytestmark = pytest.mark.gpu
 C32 = ri.COEFFS_F32
@@ -152,3 +156,67 @@ def test_binding_validates_host_arrays(P):
         with pytest.raises(ValueError):
             P.rtm_read_field(sim.h, np.empty(shape, np.float32))
         assert sim.read_field().shape == (3,) + shape
+
+
+# ----------------------------------------------------------------------------- slab data plane
+def _slabs(P, v, steps, u0, up0, src, G, halo, host_ordered=0, graphs=1, chunks=None):
+    nz, ny, nx = v.shape
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, devices=[0] * G) as sim:
+        P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, halo)
+        P.rtm_set_option(sim.h, P.RTM_OPT_HOST_ORDERED, host_ordered)
+        P.rtm_set_option(sim.h, P.RTM_OPT_GRAPHS, graphs)
+        sim.set_velocity(v)
+        for s in src:
+            sim.inject_source(*s)
+        sim.set_fields(u0, up0)
+        for k in (chunks or [steps]):
+            sim.step(k)
+        return sim.read_fields(), P.rtm_last_enqueue_ms(sim.h)
+
+
+@pytest.mark.parametrize("G,host_ordered", [(2, 0), (3, 0), (4, 0), (3, 1)])
+def test_multislab_copy_engine_pull_bitwise(P, G, host_ordered):
+    """Halo mode 3 in-process: boundary planes, 'boundary ready' flags, copy-engine pulls from
+    the neighbours' buffers on the comm streams overlapped with the interior, 'step complete'
+    flags (WAR) — bitwise equal to G = 1, through reset and resume restarts."""
+    v, u0, up0, src = _case(30 + G)
+    ref_u, ref_up = _single(P, v, 21, u0, up0, src)
+    (u, up), _ = _slabs(P, v, 21, u0, up0, src, G, 3, host_ordered, chunks=[1, 3, 17])
+    assert np.array_equal(u, ref_u) and np.array_equal(up, ref_up)
+    nz, ny, nx = v.shape
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, devices=[0] * G) as sim:
+        P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, 3)
+        sim.set_velocity(v)
+        for s in src:
+            sim.inject_source(*s)
+        sim.set_fields(u0, up0)
+        sim.step(9)
+        a, b = sim.read_fields()
+        sim.reset()
+        sim.step(5)
+        sim.set_fields(a, b)
+        P.rtm_set_step_count(sim.h, 9)
+        sim.step(12)
+        u2, up2 = sim.read_fields()
+    assert np.array_equal(u2, ref_u) and np.array_equal(up2, ref_up)
+
+
+@pytest.mark.parametrize("halo", [0, 1])
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_slab_step_graphs_bitwise_and_cheaper_to_enqueue(P, G, halo):
+    """The G > 1 step captured in CUDA graphs (16 steps per replay; halo modes 0 and 1:
+    boundary launch, events, copies, interior / the event-ordered fused push) is bitwise equal
+    to direct launches, from both parities, and costs less host time to enqueue."""
+    shape = (80, 37, 64)
+    v, u0, up0, src = _case(50 + G, shape)
+    ref_u, ref_up = _single(P, v, 70, u0, up0, src)
+    # 1 direct; 1 direct + 32 in 2 replays + 3 direct (capture); 1 direct + 32 in 2 replays
+    (u, up), t_graph = _slabs(P, v, 70, u0, up0, src, G, halo, graphs=1, chunks=[1, 36, 33])
+    assert np.array_equal(u, ref_u) and np.array_equal(up, ref_up)
+    (u, up), _ = _slabs(P, v, 70, u0, up0, src, G, halo, graphs=1, chunks=[70])
+    assert np.array_equal(u, ref_u) and np.array_equal(up, ref_up)
+    (u, up), t_direct = _slabs(P, v, 70, u0, up0, src, G, halo, graphs=0, chunks=[1, 36, 33])
+    assert np.array_equal(u, ref_u) and np.array_equal(up, ref_up)
+    print(f"G={G} halo={halo}: enqueue of 33 steps: graphs {t_graph:.3f} ms, direct {t_direct:.3f} ms")
+    if G >= 4:  # 2 replays + 1 direct step vs 33 direct steps of G slabs
+        assert t_graph < 0.5 * t_direct, (t_graph, t_direct)
