@@ -309,7 +309,9 @@ def main():
         # stream-kernel variant timed on this grid (max over ranks = MWMB), winner verified
         P.rtm_set_velocity_device(h, d_v.data_ptr())
         # two-step passes need a single-slab single-shot context and the resident kernel a
-        # single slab; elsewhere they would run their paired k_stream variant
+        # single slab; elsewhere they would run their paired k_stream variant.  The multi-step
+        # variants ("ms*") are left out: measured slower than single steps on C1-C4
+        # (profiles/sweep_r02_*.log)
         kinds = ("stream",) + (("resident",) if world == 1 else ()) + \
             (("tb2",) if world == 1 and args.shots == 1 else ())
         cands = [t for t in range(P.rtm_num_tiles()) if (P.rtm_tile_name(t) or "").startswith(kinds)]
@@ -464,6 +466,7 @@ def main():
                          "frac": round(achieved / peak, 4) if achieved else None,
                          "traffic": traffic, "peak_source": peak_src,
                          "kernel": ("k_tb2s" if two_step else "k_resident" if tile_name.startswith("resident") else
+                                    "k_stream(multi-step)" if tile_name.startswith("ms") else
                                     "k_stream" if tile_name.startswith(("stream", "tb2")) else
                                     "k_tiled" if tile_name.startswith("tma") else "k_naive")
                                    + f"<{tile_name}>", "launches": kl,

@@ -163,7 +163,8 @@ const char* rtm_tile_name(int tile_id);  /* e.g. "stream64x32k10d0"; NULL for un
  *                      evict_last policy, bit 3 plain (not evict-first) u_prev/C/u_next
  *                      accesses, bits 4-7 prefetch distance in planes, bits 8-9 L2 promotion
  *                      of the halo'd u TMA box (0 = 256B, 1 = 128B, 2 = 64B, 3 = none), bit 10
- *                      u_prev/C TMA loads with an evict_first policy
+ *                      u_prev/C TMA loads with an evict_first policy, bit 11 C TMA loads with an
+ *                      evict_last policy (C stays in L2 across steps when it fits)
  *   RTM_OPT_GRAPHS     1 (default) = capture runs of 16 steps in CUDA graphs, 0 = direct launches
  *   RTM_OPT_SHOT_ORDER batched contexts: 0 auto (shot-major when C fits in 40% of L2), 1 shot-major
  *                      (each shot's tiles co-run), 2 shot-fastest (co-running CTAs share C tiles)

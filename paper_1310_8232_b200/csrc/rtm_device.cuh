@@ -107,15 +107,19 @@ __device__ __forceinline__ void push_halo4(const StencilParams& p, int z, long l
     if (z >= p.nzl - 5 && p.push_hi) st_stream4(p.push_hi + (long long)(z - p.nzl + 5) * p.plane + col, v);
 }
 
-// Add the samples of the sources owned by this thread's 4-point column at plane z.
-__device__ __forceinline__ void add_sources(const StencilParams& p, uint64_t mask, int x, int z,
-                                            float (&out)[4]) {
+// Add the samples of the sources owned by this thread's 4-point column at plane z.  step()
+// returns the global index of the step being computed (sample n is added after the stencil of
+// step n); it is evaluated only when a source lies in plane z — a device-counter read must not
+// stall the owning warp on every plane (it would throttle the whole CTA pipeline).
+template <class StepFn>
+__device__ __forceinline__ void add_sources_f(const StencilParams& p, uint64_t mask, int x, int z,
+                                              StepFn step, float (&out)[4]) {
     while (mask) {
         const int s = __ffsll(static_cast<long long>(mask)) - 1;
         mask &= mask - 1;
         const DevSource& src = p.src[s];
         if (src.z == z) {
-            const int n = *reinterpret_cast<volatile const int*>(&p.d_step[p.parity]);
+            const int n = step();
             if (n < src.nsamples) {
                 const float w = p.samples[src.offset + n];
                 const int i = src.x - x;
@@ -126,6 +130,36 @@ __device__ __forceinline__ void add_sources(const StencilParams& p, uint64_t mas
         }
     }
 }
+// ... n known (multi-step launches: step0 + k)
+__device__ __forceinline__ void add_sources_n(const StencilParams& p, uint64_t mask, int x, int z,
+                                              int n, float (&out)[4]) {
+    add_sources_f(p, mask, x, z, [n]() { return n; }, out);
+}
+// ... n from the device step counter (graph-replayable launches)
+__device__ __forceinline__ void add_sources(const StencilParams& p, uint64_t mask, int x, int z,
+                                            float (&out)[4]) {
+    add_sources_f(p, mask, x, z,
+                  [&p]() { return *reinterpret_cast<volatile const int*>(&p.d_step[p.parity]); }, out);
+}
+
+// ---- gpu-scope acquire / release, proxy fence, watchdog (inter-CTA flags) ------------------
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+constexpr unsigned long long kWatchdogNs = 4000000000ull;
 
 __device__ __forceinline__ void mbar_wait_u32(uint32_t addr, uint32_t parity) {
     uint32_t ok;
@@ -161,7 +195,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // cache_mode (StencilParams): bits 0-1 L2 prefetch of u_prev/C (0 none, 1 evict_last,
 // 2 evict_normal); bit 2 u TMA loads with an evict_last L2 policy; bit 3 plain (not
 // evict-first) u_prev/C loads and u_next stores; bits 4-7 prefetch distance in planes;
-// bits 8-9 L2 promotion of the u box (host side); bit 10 u_prev/C TMA loads evict_first.
+// bits 8-9 L2 promotion of the u box (host side); bit 10 u_prev/C TMA loads evict_first;
+// bit 11 C TMA loads evict_last (C kept in L2 across steps where it fits).
 __device__ __forceinline__ void prefetch_l2(const void* p, int mode) {
     if (mode == 1)
         asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));

@@ -111,6 +111,9 @@ struct Slab {
     unsigned long long* d_epoch = nullptr;     // pass epoch (never reset)
     unsigned* d_bar = nullptr;                 // k_resident grid barrier [2]
     cudaGraphExec_t tb_graph[4] = {nullptr, nullptr, nullptr, nullptr};  // key bank*2 + parity
+    unsigned long long* d_msflags = nullptr;   // multi-step launches: progress flag per work unit
+    long long ms_units = 0;                    // capacity of d_msflags
+    unsigned long long ms_epoch = 0;           // per-launch tag (upper 32 bits of the flags)
     int tb_graph_variant[4] = {-1, -1, -1, -1};
     // fused halo push with the flag protocol (halo mode 2): the neighbours' time-level buffers
     // and flag words — direct pointers in-process, CUDA-IPC mappings across processes
@@ -292,6 +295,7 @@ void free_slab(Slab& s) {
         if (s.alt[b]) cudaFree(s.alt[b]);
     }
     if (s.d_flags) cudaFree(s.d_flags);
+    if (s.d_msflags) cudaFree(s.d_msflags);
     if (s.d_bar) cudaFree(s.d_bar);
     if (s.d_epoch) cudaFree(s.d_epoch);
     for (void* q : s.ipc_open) cudaIpcCloseMemHandle(q);
@@ -793,10 +797,57 @@ int step_resident(rtm_ctx* c, int nsteps) {
     return RTM_OK;
 }
 
+// Multi-step launches (kind 6): up to kMaxMsSteps time steps per cooperative launch of
+// k_stream<..., MS = true>; work units start a step once they and their face-neighbour units
+// have published the previous one (flags), instead of at a launch boundary.
+constexpr int kMaxMsSteps = 1 << 20;
+int step_mstep(rtm_ctx* c, int nsteps) {
+    Slab& s = c->slabs[0];
+    cudaStream_t st = s.stream();
+    const int var = resolve_tile(c);
+    const TileVariant& tv = variant(var);
+    RET(ensure_tmaps(c, s, var));
+    for (int k = 0; k < nsteps;) {
+        const int parity = (int)(c->step & 1);
+        StencilParams p;
+        fill_params(c, s, parity, p);
+        p.nranges = 1;
+        p.r_begin[0] = 0;
+        p.r_len[0] = s.nzl;
+        p.tiles_x = (c->nx + tv.TX - 1) / tv.TX;
+        p.tiles_y = (c->ny + tv.TY - 1) / tv.TY;
+        p.r_chunks[0] = choose_chunks(c, s.occupancy, p.tiles_x * p.tiles_y * s.nshots, s.nzl);
+        const long long units = (long long)p.tiles_x * p.tiles_y * p.r_chunks[0] * s.nshots;
+        if (units > s.ms_units) {
+            if (s.d_msflags) {
+                CK(cudaStreamSynchronize(st));
+                CK(cudaFree(s.d_msflags));
+                s.d_msflags = nullptr;
+            }
+            CK(cudaMalloc(&s.d_msflags, units * sizeof(unsigned long long)));
+            CK(cudaMemsetAsync(s.d_msflags, 0, units * sizeof(unsigned long long), st));
+            s.ms_units = units;
+        }
+        p.flags = s.d_msflags;
+        p.epoch = (++s.ms_epoch) << 32;  // flags of earlier launches are always smaller
+        p.nsteps = std::min(nsteps - k, kMaxMsSteps);
+        p.step0 = (int)c->step;
+        RET(prof_begin(c, st));
+        CK(launch_mstep(var, &s.tm_u[parity], &s.tm_in[parity ^ 1], &s.tm_u[parity ^ 1], &s.tm_in[parity],
+                        &s.tm_c, p, c->num_sms * s.occupancy, st));
+        RET(prof_end(c, st));
+        ++c->launches;
+        c->step += p.nsteps;
+        k += p.nsteps;
+    }
+    return RTM_OK;
+}
+
 int step_single(rtm_ctx* c, int nsteps) {
     Slab& s = c->slabs[0];
     cudaStream_t st = s.stream();
     if (variant(resolve_tile(c)).kind == 5) return step_resident(c, nsteps);
+    if (variant(resolve_tile(c)).kind == 6) return step_mstep(c, nsteps);
     int k = 0;
     int tb_bands = 0;
     if (variant(resolve_tile(c)).kind == 4) {
@@ -2105,7 +2156,7 @@ int rtm_set_option(rtm_ctx* c, int key, long long value) {
             c->zchunk = (int)value;
             break;
         case RTM_OPT_CACHE_MODE:
-            if (value < 0 || value > 0x7ff) return fail(RTM_EINVAL, "cache mode %lld out of range", value);
+            if (value < 0 || value > 0xfff) return fail(RTM_EINVAL, "cache mode %lld out of range", value);
             c->cache_mode = (int)value;
             break;
         case RTM_OPT_GRAPHS:

@@ -45,6 +45,14 @@ struct StencilParams {
     // neighbours' z-halo planes of their u^{n+1} buffers (peer or same-device pointers)
     float* push_lo;
     float* push_hi;
+    // multi-step launches (kind 6, k_stream<..., MS = true>): nsteps time steps in ONE
+    // cooperative launch, step k reading buf (parity + k) & 1 (u = k even ? u : next); the step
+    // index of step k is step0 + k; a unit may start step k once it and its x/y/z neighbour
+    // units have published flags[unit] >= epoch | k (epoch: a per-launch tag in the upper 32 bits)
+    int nsteps;
+    int step0;
+    unsigned long long epoch;
+    unsigned long long* flags;
     int nsrc;
     DevSource src[RTM_MAX_SOURCES];
     const float* samples;
@@ -54,7 +62,9 @@ struct TileVariant {
     const char* name;
     int kind;                  // 0 naive, 1 k_tiled (CTA per unit), 2 k_stream (persistent, producer
                                // warp), 4 k_tb2s (two time steps per HBM pass),
-                               // 5 k_resident (many steps per launch, L2-resident grids)
+                               // 5 k_resident (many steps per launch, L2-resident grids),
+                               // 6 k_stream multi-step (many steps per cooperative launch, units
+                               //   ordered by neighbour flags instead of launch boundaries)
     int TX, TY, K, D, MINB;    // tile (x, y), u ring depth, u_prev/C ring depth (0: LDG), min CTAs/SM
     int U;                     // z-loop unroll (register-queue rotation amortised over U planes)
     int KB, DB, L;             // kind 4: KB = W (store groups in flight before publication),
@@ -91,6 +101,12 @@ cudaError_t launch_variant(int id, const CUtensorMap* tm_u, const CUtensorMap* t
                            const CUtensorMap* tm_c, const StencilParams& p, int max_ctas,
                            cudaStream_t s, bool pdl = false);
 cudaError_t launch_naive(const StencilParams& p, cudaStream_t s);
+// kind 6: p.nsteps steps from buffers (p.u, p.next) in one cooperative launch; tm_u / tm_up
+// over p.u's buffer as the u box / u_prev tile at even steps (tm_u over p.u, tm_up over
+// p.next), tm_u2 / tm_up2 the same for odd steps (tm_u2 over p.next, tm_up2 over p.u).
+cudaError_t launch_mstep(int id, const CUtensorMap* tm_u, const CUtensorMap* tm_up,
+                         const CUtensorMap* tm_u2, const CUtensorMap* tm_up2, const CUtensorMap* tm_c,
+                         const StencilParams& p, int max_ctas, cudaStream_t s);
 
 // Resident multi-step kernel (kind 5, k_resident in rtm_resident.cu): nsteps time steps of a
 // single-slab context in one cooperative launch, grid barrier (bar[0..1], zeroed by the

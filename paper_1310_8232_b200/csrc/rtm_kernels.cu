@@ -309,9 +309,14 @@ __global__ void __launch_bounds__(256) k_velocity(const float* v, float* C, long
 // unit boundaries.  Work units are (z-chunk, tile) pairs, chunk-major, dealt round-robin
 // to the persistent CTAs (unit = blockIdx.x + k * gridDim.x) so co-running CTAs are xy
 // neighbours at similar z.
-template <int TX, int TY, int K, int D>
+template <int TX, int TY, int K, int D, int U = 4>
 struct StreamShape {
+    // U == 11: modulo-scheduled z queue (q[11], register names rotate with the unrolled
+    // iteration, no copies at the loop back-edge) and per-lane empty-slot arrivals (no warp
+    // sync / elected-lane branch per plane): the empty barriers count every consumer lane
+    static constexpr bool MQ = (U == 11);
     static constexpr int NW = TX * TY / 128;      // consumer warps (4 points per thread)
+    static constexpr int EMPTY_COUNT = MQ ? NW * 32 : NW;
     static constexpr int NT = NW * 32 + 32;       // + 1 producer warp
     static constexpr int TXV = TX / 4;
     static constexpr int RS = TX + 16;
@@ -363,11 +368,61 @@ __device__ __forceinline__ UnitGeom unit_geom(const StencilParams& p, int unit, 
     return g;
 }
 
-template <int TX, int TY, int K, int D, int MINB, int U>
-__global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
+// Multi-step launches (MS): the unit index of (shot, chunk, tile) — the inverse of unit_geom.
+__device__ __forceinline__ int unit_index(const StencilParams& p, int shot, int chunk, int tile) {
+    const int ntiles = p.tiles_x * p.tiles_y;
+    if (p.shot_major) return shot * ntiles * p.r_chunks[0] + chunk * ntiles + tile;
+    return (chunk * ntiles + tile) * p.nshots + shot;
+}
+// Spin (acquire, gpu scope) until flags[unit] and the flags of its face neighbours (x +- 1,
+// y +- 1 tiles of the same chunk; chunks +- 1 of the same tile; same shot) reach target, i.e.
+// until every unit whose u^{n+1} planes this unit's box reads has stored them (RAW) and has
+// finished reading the u^{n-1} planes this unit overwrites (WAR).  Then order the following
+// TMA (async-proxy) loads after the acquired generic-proxy stores.  4 s watchdog -> trap.
+__device__ __noinline__ void wait_unit_flags(const StencilParams& p, int unit, unsigned long long target) {
+    const int ntiles = p.tiles_x * p.tiles_y;
+    int shot, rest;
+    if (p.shot_major) {
+        const int per_shot = ntiles * p.r_chunks[0];
+        shot = unit / per_shot;
+        rest = unit - shot * per_shot;
+    } else {
+        shot = unit % p.nshots;
+        rest = unit / p.nshots;
+    }
+    const int chunk = rest / ntiles, tile = rest - chunk * ntiles;
+    const int ty = tile / p.tiles_x, tx = tile - ty * p.tiles_x;
+    int nb[7];
+    int m = 0;
+    nb[m++] = unit;
+    if (tx > 0) nb[m++] = unit_index(p, shot, chunk, tile - 1);
+    if (tx + 1 < p.tiles_x) nb[m++] = unit_index(p, shot, chunk, tile + 1);
+    if (ty > 0) nb[m++] = unit_index(p, shot, chunk, tile - p.tiles_x);
+    if (ty + 1 < p.tiles_y) nb[m++] = unit_index(p, shot, chunk, tile + p.tiles_x);
+    if (chunk > 0) nb[m++] = unit_index(p, shot, chunk - 1, tile);
+    if (chunk + 1 < p.r_chunks[0]) nb[m++] = unit_index(p, shot, chunk + 1, tile);
+    for (int i = 0; i < m; ++i) {
+        const unsigned long long* f = p.flags + nb[i];
+        if (ld_acquire_gpu_u64(f) >= target) continue;
+        const unsigned long long t0 = globaltimer_ns();
+        unsigned spins = 0;
+        while (ld_acquire_gpu_u64(f) < target) {
+            __nanosleep(64);
+            if ((++spins & 255) == 0 && globaltimer_ns() - t0 > kWatchdogNs) __trap();
+        }
+    }
+    fence_proxy_async_global();
+}
+
+template <int TX, int TY, int K, int D, int MINB, int U, bool MS>
+__global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
     k_stream(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_up,
-             const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ StencilParams p) {
-    using S = StreamShape<TX, TY, K, D>;
+             const __grid_constant__ CUtensorMap tm_c, const __grid_constant__ StencilParams p,
+             const __grid_constant__ CUtensorMap tm_u2, const __grid_constant__ CUtensorMap tm_up2) {
+    using S = StreamShape<TX, TY, K, D, U>;
+    constexpr bool MQ = S::MQ;
+    // queue slot of z offset k - 5 in unrolled iteration O
+    constexpr auto QI = [](int O, int k) constexpr { return MQ ? (O + k) % 11 : O + k; };
     extern __shared__ __align__(128) float smem[];
     float* uring = smem;
     float* cring = smem + K * S::USLOT;
@@ -381,11 +436,11 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
     if (tid == 0) {
         for (int k = 0; k < K; ++k) {
             mbar_init(&full_u[k], 1);
-            mbar_init(&empty_u[k], S::NW);
+            mbar_init(&empty_u[k], S::EMPTY_COUNT);
         }
         for (int k = 0; k < D; ++k) {
             mbar_init(&full_c[k], 1);
-            mbar_init(&empty_c[k], S::NW);
+            mbar_init(&empty_c[k], S::EMPTY_COUNT);
         }
         fence_mbar_init();
     }
@@ -393,22 +448,42 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
     // Programmatic dependent launch: everything above overlapped the previous grid's tail;
     // every global access below depends on it (u, u_prev, the step counter), so wait for its
     // completion here (a no-op for a normal launch), then let the next grid be scheduled.
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // (The producer lane first issues the u_prev / C tiles of its first unit: under PDL they do
+    // not depend on the previous grid — u^{n-1} was its input, not its output — so their loads
+    // overlap the previous step's tail; it waits right after.)
+    if (!(warp == S::NW && lane == 0)) asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    if (p.write_next && blockIdx.x == 0 && tid == 0)
-        p.d_step[p.parity ^ 1] = p.d_step[p.parity] + 1;
+    if constexpr (MS) {
+        // the step counter after the launch (nothing in this launch reads it: step0 + k)
+        if (blockIdx.x == 0 && tid == 0) {
+            p.d_step[(p.parity + p.nsteps) & 1] = p.step0 + p.nsteps;
+            p.d_step[(p.parity + p.nsteps + 1) & 1] = p.step0 + p.nsteps - 1;
+        }
+    } else {
+        if (p.write_next && blockIdx.x == 0 && tid == 0)
+            p.d_step[p.parity ^ 1] = p.d_step[p.parity] + 1;
+    }
 
     const int units = p.tiles_x * p.tiles_y * (p.r_chunks[0] + (p.nranges > 1 ? p.r_chunks[1] : 0)) *
                       p.nshots;
+    const int nst = MS ? p.nsteps : 1;
 
     if (warp == S::NW) {  // ---------------- producer warp
         if (lane == 0) {
             const bool hint = (p.cache_mode & 4) != 0;
             const bool chint = (p.cache_mode & 0x400) != 0;
+            const bool clast = (p.cache_mode & 0x800) != 0;
             const uint64_t pol = policy_evict_last();
             const uint64_t cpol = policy_evict_first();
             uint32_t gu = 0, gc = 0;
+            bool waited = false;  // griddepcontrol.wait done (see above)
+            for (int k = 0; k < nst; ++k)
             for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
+                const CUtensorMap* tmu = (MS && (k & 1)) ? &tm_u2 : &tm_u;
+                const CUtensorMap* tmp = (MS && (k & 1)) ? &tm_up2 : &tm_up;
+                if constexpr (MS) {
+                    if (k > 0) wait_unit_flags(p, unit, p.epoch | (unsigned long long)k);
+                }
                 const UnitGeom g = unit_geom(p, unit, TX, TY);
                 const int n = g.ze - g.zs;
                 auto put_u = [&](int j) {
@@ -416,10 +491,10 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
                     if (seq >= K) mbar_wait(&empty_u[slot], ((seq / K) - 1) & 1);
                     mbar_expect_tx(&full_u[slot], S::UBYTES);
                     if (hint)
-                        tma_load_3d_hint(uring + slot * S::USLOT, &tm_u, g.x0 - 8, g.y0 - 5,
+                        tma_load_3d_hint(uring + slot * S::USLOT, tmu, g.x0 - 8, g.y0 - 5,
                                          (int)g.soff + g.zs + j, &full_u[slot], pol);
                     else
-                        tma_load_3d(uring + slot * S::USLOT, &tm_u, g.x0 - 8, g.y0 - 5,
+                        tma_load_3d(uring + slot * S::USLOT, tmu, g.x0 - 8, g.y0 - 5,
                                     (int)g.soff + g.zs + j, &full_u[slot]);
                 };
                 auto put_c = [&](int i) {
@@ -427,24 +502,37 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
                     if (seq >= D) mbar_wait(&empty_c[slot], ((seq / D) - 1) & 1);
                     mbar_expect_tx(&full_c[slot], S::CBYTES);
                     float* dst = cring + slot * S::CSLOT;
-                    if (chint) {  // read-once streams: evict first, keep u's halo rows in L2
-                        tma_load_3d_hint(dst, &tm_up, g.x0, g.y0, (int)g.soff + g.zs + i + 5,
+                    if (chint)  // read-once stream: evict first, keep u's halo rows in L2
+                        tma_load_3d_hint(dst, tmp, g.x0, g.y0, (int)g.soff + g.zs + i + 5,
                                          &full_c[slot], cpol);
+                    else
+                        tma_load_3d(dst, tmp, g.x0, g.y0, (int)g.soff + g.zs + i + 5, &full_c[slot]);
+                    if (chint || clast)  // C: evict first (streams) or evict last (L2-resident C)
                         tma_load_3d_hint(dst + TX * TY, &tm_c, g.x0, g.y0, g.zs + i, &full_c[slot],
-                                         cpol);
-                    } else {
-                        tma_load_3d(dst, &tm_up, g.x0, g.y0, (int)g.soff + g.zs + i + 5, &full_c[slot]);
+                                         clast ? pol : cpol);
+                    else
                         tma_load_3d(dst + TX * TY, &tm_c, g.x0, g.y0, g.zs + i, &full_c[slot]);
-                    }
                 };
+                int ci = 0;  // u_prev / C planes of this unit already issued
+                if (!waited) {
+                    if constexpr (D > 0) {
+                        const int pre = n < D ? n : D;  // first ring pass: no empty-slot waits
+                        for (; ci < pre; ++ci) put_c(ci);
+                    }
+                    asm volatile("griddepcontrol.wait;" ::: "memory");
+                    waited = true;
+                }
                 for (int j = 0; j < 10; ++j) put_u(j);
                 for (int i = 0; i < n; ++i) {
-                    if constexpr (D > 0) put_c(i);
+                    if constexpr (D > 0) {
+                        if (i >= ci) put_c(i);
+                    }
                     put_u(i + 10);
                 }
                 gu += n + 10;
                 gc += n;
             }
+            if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
         }
         return;
     }
@@ -461,9 +549,13 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
     const uint32_t fc = smem_u32(full_c), ec = smem_u32(empty_c);
     const float* uown = uring + own;
     uint32_t gu = 0, gc = 0;
+    int nstep = 0;  // MS: global index of the step being computed
+    for (int k = 0; k < nst; ++k)
     for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
         const UnitGeom g = unit_geom(p, unit, TX, TY);
         const int n = g.ze - g.zs;
+        float* const nextbuf = (MS && (k & 1)) ? const_cast<float*>(p.u) : p.next;
+        if constexpr (MS) nstep = p.step0 + k;
         const int x = g.x0 + 4 * tx, y = g.y0 + ty;
         const bool active = (x < p.nx) && (y < p.ny);
         uint64_t smask = 0;
@@ -476,20 +568,25 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
             }
         }
         const long long col = (long long)y * p.pitch + x;
-        float* outp = p.next + (g.soff + g.zs + 5) * p.plane + col;  // also u_prev (D == 0)
+        float* outp = nextbuf + (g.soff + g.zs + 5) * p.plane + col;  // also u_prev (D == 0)
         const float* cp = p.C + (long long)g.zs * p.plane + col;
 
-        // register queue along z: q[O + k] = u(z - 5 + k) for the O-th unrolled iteration
-        float4 q[10 + U];
+        // register queue along z: q[QI(O, k)] = u(z - 5 + k) for the O-th unrolled iteration
+        float4 q[MQ ? 11 : 10 + U];
+        auto release_u = [&](uint32_t slot) {  // this warp is done with u-ring slot `slot`
+            if constexpr (MQ) {
+                mbar_arrive_u32(eu + 8 * slot);
+            } else {
+                __syncwarp();
+                if (lane == 0) mbar_arrive_u32(eu + 8 * slot);
+            }
+        };
 #pragma unroll
         for (int j = 0; j < 10; ++j) {
             const uint32_t seq = gu + j;
             mbar_wait_u32(fu + 8 * (seq % K), (seq / K) & 1);
             q[j] = *reinterpret_cast<const float4*>(uown + (seq % K) * S::USLOT);
-            if (j < 5) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive_u32(eu + 8 * (seq % K));
-            }
+            if (j < 5) release_u(seq % K);
         }
         // running ring positions: plane gu+i+10 (new), gu+i+5 (current), u_prev/C gc+i
         uint32_t sn = (gu + 10) % K, pn = ((gu + 10) / K) & 1;
@@ -517,7 +614,7 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
                 }
             }
             mbar_wait_u32(fu + 8 * sn, pn);
-            q[O + 10] = *reinterpret_cast<const float4*>(uown + sn * S::USLOT);
+            q[QI(O, 10)] = *reinterpret_cast<const float4*>(uown + sn * S::USLOT);
             if constexpr (D > 0) {
                 mbar_wait_u32(fc + 8 * sq, pq);
                 const float* cb = cring + sq * S::CSLOT + cown;
@@ -531,7 +628,7 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
                 const float4 rr = *reinterpret_cast<const float4*>(row + 4);
                 xs[0] = row[-5];
                 xs[1] = l.x; xs[2] = l.y; xs[3] = l.z; xs[4] = l.w;
-                xs[5] = q[O + 5].x; xs[6] = q[O + 5].y; xs[7] = q[O + 5].z; xs[8] = q[O + 5].w;
+                xs[5] = q[QI(O, 5)].x; xs[6] = q[QI(O, 5)].y; xs[7] = q[QI(O, 5)].z; xs[8] = q[QI(O, 5)].w;
                 xs[9] = rr.x; xs[10] = rr.y; xs[11] = rr.z; xs[12] = rr.w;
                 xs[13] = row[8];
             }
@@ -541,7 +638,7 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
                 yv[5 - m] = *reinterpret_cast<const float4*>(row - m * S::RS);
                 yv[5 + m] = *reinterpret_cast<const float4*>(row + m * S::RS);
             }
-            yv[5] = q[O + 5];
+            yv[5] = q[QI(O, 5)];
             float out[4];
             {
                 // x pair sums for points (0,1) and (2,3): even m are aligned register pairs
@@ -550,20 +647,20 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
                 const float4 R4 = make_float4(xs[9], xs[10], xs[11], xs[12]);
                 float2 xa[5], xb[5];
                 xa[0] = make_float2(__fadd_rn(xs[4], xs[6]), __fadd_rn(xs[5], xs[7]));
-                xa[1] = __fadd2_rn(hi2(L4), hi2(q[O + 5]));
+                xa[1] = __fadd2_rn(hi2(L4), hi2(q[QI(O, 5)]));
                 xa[2] = make_float2(__fadd_rn(xs[2], xs[8]), __fadd_rn(xs[3], xs[9]));
                 xa[3] = __fadd2_rn(lo2(L4), lo2(R4));
                 xa[4] = make_float2(__fadd_rn(xs[0], xs[10]), __fadd_rn(xs[1], xs[11]));
                 xb[0] = make_float2(__fadd_rn(xs[6], xs[8]), __fadd_rn(xs[7], xs[9]));
-                xb[1] = __fadd2_rn(lo2(q[O + 5]), lo2(R4));
+                xb[1] = __fadd2_rn(lo2(q[QI(O, 5)]), lo2(R4));
                 xb[2] = make_float2(__fadd_rn(xs[4], xs[10]), __fadd_rn(xs[5], xs[11]));
                 xb[3] = __fadd2_rn(hi2(L4), hi2(R4));
                 xb[4] = make_float2(__fadd_rn(xs[2], xs[12]), __fadd_rn(xs[3], xs[13]));
                 float2 za[11], zb[11], ya[11], yb[11];
 #pragma unroll
                 for (int o = 0; o < 11; ++o) {
-                    za[o] = lo2(q[O + o]);
-                    zb[o] = hi2(q[O + o]);
+                    za[o] = lo2(q[QI(O, o)]);
+                    zb[o] = hi2(q[QI(O, o)]);
                     ya[o] = lo2(yv[o]);
                     yb[o] = hi2(yv[o]);
                 }
@@ -571,12 +668,22 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
                 const float2 rb = rtm_point2(zb, yb, xb, hi2(upv), hi2(cv), c);
                 out[0] = ra.x; out[1] = ra.y; out[2] = rb.x; out[3] = rb.y;
             }
-            __syncwarp();
-            if (lane == 0) {
+            if constexpr (MQ) {
                 mbar_arrive_u32(eu + 8 * sc);
                 if constexpr (D > 0) mbar_arrive_u32(ec + 8 * sq);
+            } else {
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive_u32(eu + 8 * sc);
+                    if constexpr (D > 0) mbar_arrive_u32(ec + 8 * sq);
+                }
             }
-            if (smask) add_sources(p, smask, x, g.zs + it, out);
+            if (smask) {
+                if constexpr (MS)
+                    add_sources_n(p, smask, x, g.zs + it, nstep, out);
+                else
+                    add_sources(p, smask, x, g.zs + it, out);
+            }
             if (active) {
                 zero_pad(out, x, p.nx);
                 const float4 o4 = make_float4(out[0], out[1], out[2], out[3]);
@@ -598,16 +705,24 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
 #pragma unroll 1
         for (int i = 0; i < n; i += U) {
             if (!unrolled<0, U>(body, i, n)) break;
+            if constexpr (!MQ) {
 #pragma unroll
-            for (int o = 0; o < 10; ++o) q[o] = q[o + U];
+                for (int o = 0; o < 10; ++o) q[o] = q[o + U];
+            }
         }
 #pragma unroll 1
-        for (int j = n + 5; j < n + 10; ++j) {  // planes used only by the queue
-            __syncwarp();
-            if (lane == 0) mbar_arrive_u32(eu + 8 * ((gu + j) % K));
-        }
+        for (int j = n + 5; j < n + 10; ++j) release_u((gu + j) % K);  // planes used only by the queue
         gu += n + 10;
         gc += n;
+        if constexpr (MS) {
+            // publish "unit done with step k": every consumer warp's stores of the unit, then a
+            // gpu-scope release (cumulative over the CTA barrier) read by the neighbours' producers
+            asm volatile("bar.sync 1, %0;" ::"n"(S::NW * 32) : "memory");
+            if (tid == 0) {
+                __threadfence();
+                st_release_gpu_u64(p.flags + unit, p.epoch | (unsigned long long)(k + 1));
+            }
+        }
     }
 }
 
@@ -651,6 +766,23 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D>::NT, MINB)
     X(35, "stream64x30k10d6u4", 2, 64, 30, 10, 6, 1, 4)   \
     X(36, "stream64x28k10d6u11", 2, 64, 28, 10, 6, 1, 11)
 
+// Multi-step (kind 6) variants: k_stream<..., MS = true>, same columns as RTM_VARIANTS.
+// The last column is the single-step k_stream variant of the same shape, run where multi-step
+// launches do not apply (slab contexts).
+#define RTM_MS_VARIANTS(X)                                      \
+    X(43, "ms64x30k10d6u4", 6, 64, 30, 10, 6, 1, 4, 35)         \
+    X(44, "ms128x7k8d4u4", 6, 128, 7, 8, 4, 2, 4, 10)           \
+    X(45, "ms64x16k8d4u4", 6, 64, 16, 8, 4, 2, 4, 1)            \
+    X(46, "ms64x14k10d5u4", 6, 64, 14, 10, 5, 2, 4, 17)         \
+    X(47, "ms64x28k10d6u4", 6, 64, 28, 10, 6, 1, 4, 28)         \
+    X(50, "ms64x30k10d6u11", 6, 64, 30, 10, 6, 1, 11, 48)
+
+// Later single-step (kind 2) variants, appended after the multi-step ids: the U = 11 forms
+// (modulo-scheduled z queue, per-lane slot release) of the best tiles.
+#define RTM_VARIANTS2(X)                                   \
+    X(48, "stream64x30k10d6u11", 2, 64, 30, 10, 6, 1, 11)  \
+    X(49, "stream128x7k8d4u11", 2, 128, 7, 8, 4, 2, 11)
+
 static const TileVariant kVariants[] = {
     {"naive", 0, 0, 0, 0, 0, 0, 1, 0, 0, 0, 0},
 #define X(id, name, kind, tx, ty, k, d, mb, u) {name, kind, tx, ty, k, d, mb, u, 0, 0, 0, 0},
@@ -661,6 +793,19 @@ static const TileVariant kVariants[] = {
 #undef X
 #define X(id, name, threads, per_sm, pair) {name, 5, threads, 0, 0, 0, per_sm, 1, 0, 0, 0, pair},
     RTM_RESIDENT_VARIANTS(X)
+#undef X
+// (table order = id order: 43-47 multi-step, 48-49 single-step, 50 multi-step)
+#define X(id, name, kind, tx, ty, k, d, mb, u, pair) \
+    {name, kind, tx, ty, k, d, mb, u, 0, 0, 0, pair},
+#define X2(id, name, kind, tx, ty, k, d, mb, u) {name, kind, tx, ty, k, d, mb, u, 0, 0, 0, 0},
+    X(43, "ms64x30k10d6u4", 6, 64, 30, 10, 6, 1, 4, 35)
+    X(44, "ms128x7k8d4u4", 6, 128, 7, 8, 4, 2, 4, 10)
+    X(45, "ms64x16k8d4u4", 6, 64, 16, 8, 4, 2, 4, 1)
+    X(46, "ms64x14k10d5u4", 6, 64, 14, 10, 5, 2, 4, 17)
+    X(47, "ms64x28k10d6u4", 6, 64, 28, 10, 6, 1, 4, 28)
+    RTM_VARIANTS2(X2)
+    X(50, "ms64x30k10d6u11", 6, 64, 30, 10, 6, 1, 11, 48)
+#undef X2
 #undef X
 };
 
@@ -675,8 +820,8 @@ static cudaError_t prepare(const void** fn, int* threads, size_t* smem) {
         *threads = S::NT;
         *smem = S::SMEM;
     } else {
-        using S = StreamShape<TX, TY, K, D>;
-        *fn = reinterpret_cast<const void*>(&k_stream<TX, TY, K, D, MINB, U>);
+        using S = StreamShape<TX, TY, K, D, U>;
+        *fn = reinterpret_cast<const void*>(&k_stream<TX, TY, K, D, MINB, U, KIND == 6>);
         *threads = S::NT;
         *smem = S::SMEM;
     }
@@ -697,6 +842,16 @@ static cudaError_t variant_fn(int id, const void** fn, int* threads, size_t* sme
     case vid:                                   \
         return prepare<kind, tx, ty, k, d, mb, u>(fn, threads, smem);
         RTM_VARIANTS(X)
+#undef X
+#define X(vid, name, kind, tx, ty, k, d, mb, u, pair) \
+    case vid:                                         \
+        return prepare<kind, tx, ty, k, d, mb, u>(fn, threads, smem);
+        RTM_MS_VARIANTS(X)
+#undef X
+#define X(vid, name, kind, tx, ty, k, d, mb, u) \
+    case vid:                                   \
+        return prepare<kind, tx, ty, k, d, mb, u>(fn, threads, smem);
+        RTM_VARIANTS2(X)
 #undef X
         default:
             return cudaErrorInvalidValue;
@@ -735,7 +890,7 @@ cudaError_t launch_variant(int id, const CUtensorMap* tm_u, const CUtensorMap* t
     const void* fn;
     int threads;
     size_t smem;
-    if (variant(id).kind >= 3) return cudaErrorInvalidValue;  // two-step passes: launch_tb2s
+    if (variant(id).kind >= 3) return cudaErrorInvalidValue;  // two-step / multi-step: own launchers
     cudaError_t e = variant_fn(id, &fn, &threads, &smem);
     if (e != cudaSuccess) return e;
     const long long units = (long long)p.tiles_x * p.tiles_y *
@@ -747,7 +902,8 @@ cudaError_t launch_variant(int id, const CUtensorMap* tm_u, const CUtensorMap* t
     }
     const long long grid = units < max_ctas ? units : max_ctas;
     void* args[] = {const_cast<CUtensorMap*>(tm_u), const_cast<CUtensorMap*>(tm_up),
-                    const_cast<CUtensorMap*>(tm_c), const_cast<StencilParams*>(&p)};
+                    const_cast<CUtensorMap*>(tm_c), const_cast<StencilParams*>(&p),
+                    const_cast<CUtensorMap*>(tm_u), const_cast<CUtensorMap*>(tm_up)};
     if (!pdl) return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(threads), args, smem, s);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(grid));
@@ -760,6 +916,25 @@ cudaError_t launch_variant(int id, const CUtensorMap* tm_u, const CUtensorMap* t
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+cudaError_t launch_mstep(int id, const CUtensorMap* tm_u, const CUtensorMap* tm_up,
+                         const CUtensorMap* tm_u2, const CUtensorMap* tm_up2, const CUtensorMap* tm_c,
+                         const StencilParams& p, int max_ctas, cudaStream_t s) {
+    if (variant(id).kind != 6 || p.nranges != 1 || !p.flags || p.nsteps < 1) return cudaErrorInvalidValue;
+    const void* fn;
+    int threads;
+    size_t smem;
+    cudaError_t e = variant_fn(id, &fn, &threads, &smem);
+    if (e != cudaSuccess) return e;
+    const long long units = (long long)p.tiles_x * p.tiles_y * p.r_chunks[0] * p.nshots;
+    if (units <= 0) return cudaSuccess;
+    // every CTA must be co-resident: units wait on their neighbours' flags (cooperative launch)
+    const long long grid = units < max_ctas ? units : max_ctas;
+    void* args[] = {const_cast<CUtensorMap*>(tm_u), const_cast<CUtensorMap*>(tm_up),
+                    const_cast<CUtensorMap*>(tm_c), const_cast<StencilParams*>(&p),
+                    const_cast<CUtensorMap*>(tm_u2), const_cast<CUtensorMap*>(tm_up2)};
+    return cudaLaunchCooperativeKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(threads), args, smem, s);
 }
 
 cudaError_t launch_naive(const StencilParams& p, cudaStream_t s) {

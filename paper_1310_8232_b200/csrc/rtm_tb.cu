@@ -32,25 +32,6 @@
 
 namespace rtm {
 
-// ---- gpu/cta-scope acquire/release, proxy fence, watchdog --------------------------------
-__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_gpu_u64(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_global() {
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-constexpr unsigned long long kWatchdogNs = 4000000000ull;
-
 // mbarrier wait with a watchdog on the slow path only
 __device__ __forceinline__ void mbar_wait_wd(uint32_t addr, uint32_t parity) {
     uint32_t ok;

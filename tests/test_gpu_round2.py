@@ -220,3 +220,81 @@ def test_slab_step_graphs_bitwise_and_cheaper_to_enqueue(P, G, halo):
     print(f"G={G} halo={halo}: enqueue of 33 steps: graphs {t_graph:.3f} ms, direct {t_direct:.3f} ms")
     if G >= 4:  # 2 replays + 1 direct step vs 33 direct steps of G slabs
         assert t_graph < 0.5 * t_direct, (t_graph, t_direct)
+
+
+# ----------------------------------------------------------------------------- multi-step (kind 6)
+def _ms_ids(P):
+    return [t for t in range(P.rtm_num_tiles()) if (P.rtm_tile_name(t) or "").startswith("ms")]
+
+
+def _run_tile(P, v, chunks, u0, up0, src, tile, zchunk=0, shots=1, order=0, profiling=0):
+    nz, ny, nx = v.shape
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, shots=shots) as sim:
+        sim.set_tile(tile)
+        P.rtm_set_zchunk(sim.h, zchunk)
+        P.rtm_set_option(sim.h, P.RTM_OPT_SHOT_ORDER, order)
+        P.rtm_set_profiling(sim.h, profiling)
+        sim.set_velocity(v)
+        for k in range(shots):
+            for (x, y, z, w) in src:
+                P.rtm_inject_source_shot(sim.h, k, (x + 7 * k) % nx, y, z, w)
+        if u0 is not None:
+            sim.set_fields(np.stack([u0] * shots) if shots > 1 else u0,
+                           np.stack([up0] * shots) if shots > 1 else up0)
+        for c in chunks:
+            sim.step(c)
+        return sim.read_fields(), P.rtm_launch_count(sim.h)
+
+
+@pytest.mark.parametrize("zchunk", [0, 6, 11])
+def test_multistep_launch_bitwise_equals_single_steps(P, zchunk):
+    """k_stream<..., MS> runs many time steps in ONE cooperative launch, each work unit waiting
+    only for its face-neighbour units' flags: the bits equal one k_stream launch per step
+    (ragged grid, sources on tile / chunk edges and the z ends, odd starts, 1-step calls)."""
+    shape = (45, 67, 100)
+    rng = np.random.default_rng(404)
+    v = rng.uniform(1500, 4300, shape).astype(np.float32)
+    u0, up0 = ri.random_fields(shape, seed=404)
+    w = ri.source_samples(3000.0, 1e-3, 15.0, 60)
+    src = [(0, 0, 0, w), (99, 66, 44, -w), (63, 29, 11, w), (64, 30, 12, 0.5 * w), (31, 7, 22, w),
+           (32, 60, 33, -w)]
+    ref, _ = _run_tile(P, v, [37], u0, up0, src, 35, zchunk=zchunk)
+    for t in _ms_ids(P):
+        for chunks in ([37], [1, 1, 35], [3, 34]):
+            got, launches = _run_tile(P, v, chunks, u0, up0, src, t, zchunk=zchunk)
+            assert np.array_equal(got[0], ref[0]), (P.rtm_tile_name(t), chunks)
+            assert np.array_equal(got[1], ref[1]), (P.rtm_tile_name(t), chunks)
+            assert launches == len(chunks)  # one launch per rtm_step call
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_multistep_batched_shots_bitwise(P, order):
+    shape = (30, 40, 64)
+    rng = np.random.default_rng(9)
+    v = rng.uniform(1500, 4300, shape).astype(np.float32)
+    w = ri.source_samples(3000.0, 1e-3, 15.0, 40)
+    src = [(20, 20, 15, w), (3, 39, 29, -w)]
+    ref, _ = _run_tile(P, v, [23], None, None, src, 1, shots=3, order=order)
+    for t in _ms_ids(P)[:2]:
+        got, _ = _run_tile(P, v, [4, 19], None, None, src, t, shots=3, order=order)
+        assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1]), P.rtm_tile_name(t)
+
+
+def test_multistep_c2_full_run_vs_oracle_and_profiled(P):
+    """C2 (256^3, 500 steps) with the multi-step kernel: within the north-star tolerance of the
+    fp32 oracle, bitwise equal to per-step launches; the profiled path (events around each
+    launch) gives the same bits."""
+    import oracle
+    cfg = ri.make_config(2)
+    v = cfg.velocity()
+    src = cfg.sources()
+    ms = _ms_ids(P)[0]
+    got, launches = _run_tile(P, v, [cfg.steps], None, None, src, ms)
+    assert launches == 1
+    ref, _ = _run_tile(P, v, [cfg.steps], None, None, src, 35)
+    assert np.array_equal(got[0], ref[0])
+    prof, _ = _run_tile(P, v, [cfg.steps], None, None, src, ms, profiling=1)
+    assert np.array_equal(prof[0], ref[0])
+    orc = oracle.run(v, cfg.dx, cfg.dt, C32, cfg.steps, sources=src)
+    m = float(np.abs(orc).max())
+    assert float(np.abs(got[0].astype(np.float64) - orc).max()) <= 1e-4 * m
