@@ -167,6 +167,7 @@ struct rtm_ctx {
     std::vector<HostSource> sources;
     bool profiling = false;
     std::vector<cudaEvent_t> prof_ev;
+    std::vector<int> prof_weight;       // stencil launches between each event pair (graph: 16)
     long long prof_launches = 0;        // event pairs recorded in the current rtm_step
     long long prof_total_launches = 0;  // since rtm_set_profiling / last rtm_kernel_stats
     double prof_ms = 0;
@@ -512,6 +513,8 @@ int launch_stencil(rtm_ctx* c, Slab& s, int parity, int b0, int l0, int b1, int 
     }
     if (c->profiling) {
         CK(cudaEventRecord(e1, st));
+        if (c->prof_weight.size() <= (size_t)c->prof_launches) c->prof_weight.resize(c->prof_launches + 1);
+        c->prof_weight[c->prof_launches] = 1;
         ++c->prof_launches;
     }
     ++c->launches;
@@ -524,8 +527,8 @@ int collect_profile(rtm_ctx* c) {
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, c->prof_ev[2 * k], c->prof_ev[2 * k + 1]));
         c->prof_ms += ms;
+        c->prof_total_launches += c->prof_weight[k];
     }
-    c->prof_total_launches += c->prof_launches;
     return RTM_OK;
 }
 
@@ -537,9 +540,12 @@ int build_graph(rtm_ctx* c, Slab& s) {
     RET(ensure_tmaps(c, s, var));
     CK(cudaStreamBeginCapture(s.s_own, cudaStreamCaptureModeThreadLocal));
     const long long saved = c->launches;
+    const bool prof = c->profiling;  // per-launch events stay outside the capture
+    c->profiling = false;
     int rc = RTM_OK;
     for (int k = 0; k < 2 * GRAPH_PAIRS && rc == RTM_OK; ++k)
         rc = launch_stencil(c, s, k & 1, 0, s.nzl, 0, 0, 1, s.s_own);
+    c->profiling = prof;
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(s.s_own, &g);
     c->launches = saved;
@@ -576,9 +582,11 @@ int prof_begin(rtm_ctx* c, cudaStream_t st) {
     CK(cudaEventRecord(c->prof_ev[k], st));
     return RTM_OK;
 }
-int prof_end(rtm_ctx* c, cudaStream_t st) {
+int prof_end(rtm_ctx* c, cudaStream_t st, int weight = 1) {
     if (!c->profiling) return RTM_OK;
     CK(cudaEventRecord(c->prof_ev[2 * (size_t)c->prof_launches + 1], st));
+    if (c->prof_weight.size() <= (size_t)c->prof_launches) c->prof_weight.resize(c->prof_launches + 1);
+    c->prof_weight[c->prof_launches] = weight;
     ++c->prof_launches;
     return RTM_OK;
 }
@@ -870,9 +878,13 @@ int step_single(rtm_ctx* c, int nsteps) {
             k += 2 * passes;
             continue;
         }
-        if (c->graphs && !c->profiling && parity == 0 && nsteps - k >= 2 * GRAPH_PAIRS) {
+        if (c->graphs && parity == 0 && nsteps - k >= 2 * GRAPH_PAIRS) {
+            // profiling: one event pair around the replay (16 launches, back to back on the
+            // device), so short launches are timed without breaking the graph
             RET(build_graph(c, s));
+            RET(prof_begin(c, st));
             CK(cudaGraphLaunch(s.graph, st));
+            RET(prof_end(c, st, 2 * GRAPH_PAIRS));
             c->step += 2 * GRAPH_PAIRS;
             c->launches += 2 * GRAPH_PAIRS;
             k += 2 * GRAPH_PAIRS;

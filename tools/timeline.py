@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--halo", type=int, default=0)
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--tile", type=int, default=35)
+    ap.add_argument("--graphs", type=int, default=0)
     ap.add_argument("--out", default="")
     ap.add_argument("--trace", default="", help="also write the raw chrome trace here")
     a = ap.parse_args()
@@ -33,14 +34,17 @@ def main():
     import rtm_inputs as ri
     cfg = ri.make_config(a.config)
     v = cfg.velocity()
-    h = P.rtm_create_multi(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32, [0] * a.slabs)
-    P.rtm_set_option(h, P.RTM_OPT_HALO_MODE, a.halo)
-    P.rtm_set_option(h, P.RTM_OPT_GRAPHS, 0)  # direct launches: one trace entry per operation
+    if a.slabs > 1:
+        h = P.rtm_create_multi(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32, [0] * a.slabs)
+        P.rtm_set_option(h, P.RTM_OPT_HALO_MODE, a.halo)
+    else:
+        h = P.rtm_create(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32)
+    P.rtm_set_option(h, P.RTM_OPT_GRAPHS, a.graphs)  # 0: one trace entry per direct launch
     P.rtm_set_tile(h, a.tile)
     P.rtm_set_velocity(h, v)
     for s in cfg.sources(v):
         P.rtm_inject_source(h, *s)
-    P.rtm_step(h, 6)
+    P.rtm_step(h, 36)  # warm-up (tensor maps, graphs)
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         P.rtm_step(h, a.steps)
@@ -82,12 +86,18 @@ def main():
     copy_t = sum(c["t1_us"] - c["t0_us"] for c in copies)
     ov = sum(overlap(c) for c in copies)
     span = ev[-1]["t1_us"]
+    # consecutive stencil launches: device gap between the end of one and the start of the next
+    gaps = [b["t0_us"] - a_["t1_us"] for a_, b in zip(stencils, stencils[1:])]
+    kd = [x["t1_us"] - x["t0_us"] for x in stencils]
     res = {"config": f"C{cfg.k}", "grid": [cfg.nx, cfg.ny, cfg.nz], "slabs": a.slabs, "halo": a.halo,
            "tile": P.rtm_tile_name(a.tile), "steps": a.steps, "span_us": round(span, 1),
            "us_per_step": round(span / a.steps, 1), "stencil_launches": len(stencils),
            "interior_launches": len(interior), "copies": len(copies),
            "copy_us_total": round(copy_t, 1), "copy_us_overlapped_by_interior": round(ov, 1),
            "overlap_frac": round(ov / copy_t, 3) if copy_t else None,
+           "stencil_us_mean": round(sum(kd) / len(kd), 2) if kd else None,
+           "gap_us_mean": round(sum(gaps) / len(gaps), 2) if gaps else None,
+           "gap_us_max": round(max(gaps), 2) if gaps else None,
            "source": "torch.profiler (CUPTI activity records: device timestamps)",
            "events": [{k: (round(v, 2) if isinstance(v, float) else v) for k, v in x.items()}
                       for x in ev[:400]]}
