@@ -52,9 +52,10 @@ def parse():
     ap.add_argument("--nsteps", type=int, default=0, help="override the config's time steps")
     ap.add_argument("--shots", type=int, default=1,
                     help="batched independent shots on the config's velocity model (f3)")
-    ap.add_argument("--halo", type=int, default=0, choices=[0, 2],
+    ap.add_argument("--halo", type=int, default=0, choices=[0, 2, 3],
                     help="N > 1 halo exchange: 0 NCCL send/recv (default), 2 fused push over "
-                         "CUDA-IPC peer stores + flag protocol (SURVEY §8(f) f1)")
+                         "CUDA-IPC peer stores + flag protocol (SURVEY §8(f) f1), 3 copy-engine "
+                         "pull from CUDA-IPC mappings + flag protocol (SURVEY §8(e))")
     ap.add_argument("--pdl", type=int, default=-1, choices=[-1, 0, 1],
                     help="programmatic dependent launch of consecutive steps (-1: library default)")
     ap.add_argument("--no-e2e", action="store_true")
