@@ -162,6 +162,7 @@ struct rtm_ctx {
     int check_every = 0;    // NaN/Inf scan every k steps (0 = off)
     int tb_ctas = 0;        // two-step passes: max CTAs per band (0 = #SMs)
     bool pdl = false;       // programmatic dependent launch of consecutive k_stream steps
+    int zdir = 0;           // RTM_OPT_ZDIR: 1 = k_stream sweeps z downward on odd-parity steps
     int l2_bytes = 0;
     bool graphs = true;
     std::vector<HostSource> sources;
@@ -464,6 +465,7 @@ void fill_params(const rtm_ctx* c, const Slab& s, int parity, StencilParams& p) 
     for (int k = 0; k < p.nsrc; ++k) p.src[k] = s.srcs[k];
     p.samples = s.d_samples;
     p.cache_mode = c->cache_mode;
+    p.zalt = c->zdir;
     // auto: shot-major when one C field fits comfortably in L2 (it is then re-read from L2 by
     // every shot and the shots keep the full co-running tile set for halo reuse); otherwise
     // shot-fastest so co-running CTAs share each C tile
@@ -2194,6 +2196,10 @@ int rtm_set_option(rtm_ctx* c, int key, long long value) {
             if (value < 0 || value > 1) return fail(RTM_EINVAL, "host ordered %lld not in 0..1", value);
             c->host_ordered = value != 0;
             break;
+        case RTM_OPT_ZDIR:
+            if (value < 0 || value > 1) return fail(RTM_EINVAL, "z direction mode %lld not in 0..1", value);
+            c->zdir = (int)value;
+            break;
         case RTM_OPT_HALO_MODE:
             if (value < 0 || value > 3) return fail(RTM_EINVAL, "halo mode %lld not in 0..3", value);
             if (value == 0 && c->mode == 3 && c->world > 1)
@@ -2240,6 +2246,7 @@ long long rtm_get_option(rtm_ctx* c, int key) {
         case RTM_OPT_TB_CTAS: return c->tb_ctas;
         case RTM_OPT_PDL: return c->pdl ? 1 : 0;
         case RTM_OPT_HOST_ORDERED: return c->host_ordered ? 1 : 0;
+        case RTM_OPT_ZDIR: return c->zdir;
         default: return -1;
     }
 }

@@ -486,32 +486,38 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
                 }
                 const UnitGeom g = unit_geom(p, unit, TX, TY);
                 const int n = g.ze - g.zs;
+                // z sweep direction of this step (RTM_OPT_ZDIR): down on odd-parity steps, so a
+                // step starts on the planes the previous step touched last (still in L2).
+                // Buffer plane of sweep position j of the u box / of output i (u_prev tile):
+                const bool down = p.zalt && (((MS ? p.parity + k : p.parity) & 1) != 0);
+                const int ub0 = (int)g.soff + (down ? g.ze + 9 : g.zs), ustep = down ? -1 : 1;
+                const int cz0 = down ? g.ze - 1 : g.zs;
                 auto put_u = [&](int j) {
                     const uint32_t seq = gu + j, slot = seq % K;
                     if (seq >= K) mbar_wait(&empty_u[slot], ((seq / K) - 1) & 1);
                     mbar_expect_tx(&full_u[slot], S::UBYTES);
                     if (hint)
                         tma_load_3d_hint(uring + slot * S::USLOT, tmu, g.x0 - 8, g.y0 - 5,
-                                         (int)g.soff + g.zs + j, &full_u[slot], pol);
+                                         ub0 + ustep * j, &full_u[slot], pol);
                     else
                         tma_load_3d(uring + slot * S::USLOT, tmu, g.x0 - 8, g.y0 - 5,
-                                    (int)g.soff + g.zs + j, &full_u[slot]);
+                                    ub0 + ustep * j, &full_u[slot]);
                 };
                 auto put_c = [&](int i) {
                     const uint32_t seq = gc + i, slot = seq % D;
                     if (seq >= D) mbar_wait(&empty_c[slot], ((seq / D) - 1) & 1);
                     mbar_expect_tx(&full_c[slot], S::CBYTES);
                     float* dst = cring + slot * S::CSLOT;
+                    const int cz = cz0 + ustep * i;  // owned plane of output i
                     if (chint)  // read-once stream: evict first, keep u's halo rows in L2
-                        tma_load_3d_hint(dst, tmp, g.x0, g.y0, (int)g.soff + g.zs + i + 5,
-                                         &full_c[slot], cpol);
+                        tma_load_3d_hint(dst, tmp, g.x0, g.y0, (int)g.soff + cz + 5, &full_c[slot], cpol);
                     else
-                        tma_load_3d(dst, tmp, g.x0, g.y0, (int)g.soff + g.zs + i + 5, &full_c[slot]);
+                        tma_load_3d(dst, tmp, g.x0, g.y0, (int)g.soff + cz + 5, &full_c[slot]);
                     if (chint || clast)  // C: evict first (streams) or evict last (L2-resident C)
-                        tma_load_3d_hint(dst + TX * TY, &tm_c, g.x0, g.y0, g.zs + i, &full_c[slot],
+                        tma_load_3d_hint(dst + TX * TY, &tm_c, g.x0, g.y0, cz, &full_c[slot],
                                          clast ? pol : cpol);
                     else
-                        tma_load_3d(dst + TX * TY, &tm_c, g.x0, g.y0, g.zs + i, &full_c[slot]);
+                        tma_load_3d(dst + TX * TY, &tm_c, g.x0, g.y0, cz, &full_c[slot]);
                 };
                 int ci = 0;  // u_prev / C planes of this unit already issued
                 if (!waited) {
@@ -568,8 +574,14 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
             }
         }
         const long long col = (long long)y * p.pitch + x;
-        float* outp = nextbuf + (g.soff + g.zs + 5) * p.plane + col;  // also u_prev (D == 0)
-        const float* cp = p.C + (long long)g.zs * p.plane + col;
+        // sweep direction (see the producer); the z register queue is filled in sweep order, so
+        // a downward sweep mirrors it — the z pair sums u(z-m) + u(z+m) are commutative (IEEE
+        // addition), so results are bitwise those of the upward sweep
+        const bool down = p.zalt && (((MS ? p.parity + k : p.parity) & 1) != 0);
+        const int z0 = down ? g.ze - 1 : g.zs, zstep = down ? -1 : 1;
+        const long long pstep = down ? -p.plane : p.plane;
+        float* outp = nextbuf + (g.soff + z0 + 5) * p.plane + col;  // also u_prev (D == 0)
+        const float* cp = p.C + (long long)z0 * p.plane + col;
 
         // register queue along z: q[QI(O, k)] = u(z - 5 + k) for the O-th unrolled iteration
         float4 q[MQ ? 11 : 10 + U];
@@ -605,11 +617,11 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
             float4 upn = upv, cn = cv;
             if constexpr (D == 0) {
                 if (active && it + 1 < n) {
-                    upn = ld_mode4(outp + p.plane, plain);
-                    cn = ld_mode4(cp + p.plane, plain);
+                    upn = ld_mode4(outp + pstep, plain);
+                    cn = ld_mode4(cp + pstep, plain);
                     if (pf_mode && it + pf_dist < n) {
-                        prefetch_l2(outp + pf_dist * p.plane, pf_mode);
-                        prefetch_l2(cp + pf_dist * p.plane, pf_mode);
+                        prefetch_l2(outp + pf_dist * pstep, pf_mode);
+                        prefetch_l2(cp + pf_dist * pstep, pf_mode);
                     }
                 }
             }
@@ -680,15 +692,15 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
             }
             if (smask) {
                 if constexpr (MS)
-                    add_sources_n(p, smask, x, g.zs + it, nstep, out);
+                    add_sources_n(p, smask, x, z0 + zstep * it, nstep, out);
                 else
-                    add_sources(p, smask, x, g.zs + it, out);
+                    add_sources(p, smask, x, z0 + zstep * it, out);
             }
             if (active) {
                 zero_pad(out, x, p.nx);
                 const float4 o4 = make_float4(out[0], out[1], out[2], out[3]);
                 st_mode4(outp, o4, plain);
-                if (p.push_lo || p.push_hi) push_halo4(p, g.zs + it, col, o4);
+                if (p.push_lo || p.push_hi) push_halo4(p, z0 + zstep * it, col, o4);
             }
             if (++sn == K) sn = 0, pn ^= 1;
             if (++sc == K) sc = 0;
@@ -698,8 +710,8 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
                 upv = upn;
                 cv = cn;
             }
-            outp += p.plane;
-            cp += p.plane;
+            outp += pstep;
+            cp += pstep;
             ++it;
         };
 #pragma unroll 1

@@ -298,3 +298,51 @@ def test_multistep_c2_full_run_vs_oracle_and_profiled(P):
     orc = oracle.run(v, cfg.dx, cfg.dt, C32, cfg.steps, sources=src)
     m = float(np.abs(orc).max())
     assert float(np.abs(got[0].astype(np.float64) - orc).max()) <= 1e-4 * m
+
+
+# ----------------------------------------------------------------------------- z sweep direction
+def test_alternating_z_sweep_is_bitwise(P):
+    """RTM_OPT_ZDIR = 1: k_stream sweeps z downward on odd-parity steps (the register queue is
+    filled in sweep order; the z pair sums are commutative), bitwise equal to upward sweeps for
+    every k_stream variant (single- and multi-step), with z-chunks, sources and odd starts."""
+    shape = (41, 45, 76)
+    rng = np.random.default_rng(808)
+    v = rng.uniform(1500, 4300, shape).astype(np.float32)
+    u0, up0 = ri.random_fields(shape, seed=808)
+    w = ri.source_samples(3000.0, 1e-3, 15.0, 40)
+    src = [(0, 0, 0, w), (75, 44, 40, -w), (33, 20, 13, w), (34, 21, 27, 0.5 * w)]
+    nz, ny, nx = shape
+    ref, _ = _run_tile(P, v, [19], u0, up0, src, 35)
+    ids = [t for t in range(1, P.rtm_num_tiles()) if (P.rtm_tile_name(t) or "").startswith(("stream", "ms"))]
+    for t in ids:
+        for zc in (0, 7):
+            with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32) as sim:
+                sim.set_tile(t)
+                P.rtm_set_zchunk(sim.h, zc)
+                P.rtm_set_option(sim.h, P.RTM_OPT_ZDIR, 1)
+                sim.set_velocity(v)
+                for s in src:
+                    sim.inject_source(*s)
+                sim.set_fields(u0, up0)
+                sim.step(1)
+                sim.step(18)
+                u, up = sim.read_fields()
+            assert np.array_equal(u, ref[0]) and np.array_equal(up, ref[1]), (P.rtm_tile_name(t), zc)
+
+
+@pytest.mark.parametrize("halo", [0, 1, 2, 3])
+def test_alternating_z_sweep_with_slabs_is_bitwise(P, halo):
+    v, u0, up0, src = _case(91)
+    ref_u, ref_up = _single(P, v, 20, u0, up0, src)
+    nz, ny, nx = v.shape
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, devices=[0, 0, 0]) as sim:
+        P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, halo)
+        P.rtm_set_option(sim.h, P.RTM_OPT_ZDIR, 1)
+        sim.set_velocity(v)
+        for s in src:
+            sim.inject_source(*s)
+        sim.set_fields(u0, up0)
+        sim.step(3)
+        sim.step(17)
+        u, up = sim.read_fields()
+    assert np.array_equal(u, ref_u) and np.array_equal(up, ref_up)

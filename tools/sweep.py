@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--halo", type=int, default=0, help="RTM_OPT_HALO_MODE for --slabs > 1")
     ap.add_argument("--graphs", type=int, default=1, help="RTM_OPT_GRAPHS (CUDA-graph replays)")
     ap.add_argument("--pdl", default="0", help="comma list of RTM_OPT_PDL values (interleaved)")
+    ap.add_argument("--zdir", default="0", help="comma list of RTM_OPT_ZDIR values (interleaved)")
     args = ap.parse_args()
     import torch
     import paper_1310_8232_b200 as P
@@ -52,11 +53,13 @@ def main():
     tiles = [int(t) for t in args.tiles.split(",")] if args.tiles else list(range(P.rtm_num_tiles()))
     res = []
     for t in [t for _ in range(args.repeat) for t in tiles]:
-        for zc, cm, so, pdl in [(int(z), c, int(o), int(q)) for z in args.zchunk.split(",")
-                                for c in ([int(x, 0) for x in args.cache.split(",")] if args.cache else [None])
-                                for o in args.shot_order.split(",") for q in args.pdl.split(",")]:
+        for zc, cm, so, pdl, zd in [(int(z), c, int(o), int(q), int(d)) for z in args.zchunk.split(",")
+                                    for c in ([int(x, 0) for x in args.cache.split(",")] if args.cache else [None])
+                                    for o in args.shot_order.split(",") for q in args.pdl.split(",")
+                                    for d in args.zdir.split(",")]:
             P.rtm_set_option(h, P.RTM_OPT_SHOT_ORDER, so)
             P.rtm_set_option(h, P.RTM_OPT_PDL, pdl)
+            P.rtm_set_option(h, P.RTM_OPT_ZDIR, zd)
             P.rtm_set_tile(h, t)
             P.rtm_set_zchunk(h, zc)
             if cm is not None:
@@ -75,6 +78,7 @@ def main():
                 ms = P.rtm_last_elapsed_ms(h) / args.ni
             gpts = cfg.points * args.shots / ms / 1e6
             r = {"tile": t, "name": P.rtm_tile_name(t), "zchunk": zc, "shot_order": so, "pdl": pdl,
+                 "zdir": zd,
                  "slabs": args.slabs, "halo": args.halo, "graphs": args.graphs,
                  "enqueue_ms_per_step": round(P.rtm_last_enqueue_ms(h) / args.ni, 4),
                  "cache": hex(P.rtm_get_option(h, P.RTM_OPT_CACHE_MODE)), "ms_per_step": round(ms, 4),
@@ -83,7 +87,7 @@ def main():
             print(json.dumps(r), flush=True)
     agg = {}
     for r in res:
-        k = (r["tile"], r["zchunk"], r["cache"], r["shot_order"], r["pdl"])
+        k = (r["tile"], r["zchunk"], r["cache"], r["shot_order"], r["pdl"], r["zdir"])
         if k not in agg or r["ms_per_step"] < agg[k]["ms_per_step"]:
             agg[k] = r
     for r in sorted(agg.values(), key=lambda r: r["ms_per_step"]):
