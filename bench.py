@@ -320,9 +320,12 @@ def main():
         if args.lattice > 1:  # the paper's nC = |tiles| x |b_z| candidates (selection phase)
             lat = P.rtm_blocksize_lattice(nzl, args.lattice)
             cands, zcs = [t for t in cands for _ in lat], [z for _ in cands for z in lat]
-        res, times = P.rtm_autotune(h, args.tune_ni, tiles=cands, zchunks=zcs)
+        # nI scaled so every candidate's timed window is ~>= 30 ms on small grids (8 steps of C2
+        # are 0.4 ms: too short to rank variants 1-2 % apart); C3-C5 keep --tune-ni
+        nI = int(min(400, max(args.tune_ni, 4e9 // pts_local)))
+        res, times = P.rtm_autotune(h, nI, tiles=cands, zchunks=zcs)
         tune = {"selected": P.rtm_tile_name(res["best_tile"]), "candidates": len(cands),
-                "nI": args.tune_ni, "min_time_ms": round(res["min_time_ms"], 4),
+                "nI": nI, "min_time_ms": round(res["min_time_ms"], 4),
                 "zchunk": res.get("best_zchunk"), "lattice_P": args.lattice or None,
                 "actual_time_ms": round(res["actual_time_ms"], 4),
                 "quality_pct": round(res["quality_pct"], 2)}
@@ -370,10 +373,12 @@ def main():
     clocks = ClockSampler(local)
     with clocks:
         barrier()
+        torch.cuda.nvtx.range_push("bench_timed")  # ncu --nvtx --nvtx-include bench_timed/
         e0.record(stream)
         for _ in range(args.steps):
             kernel_step()
         e1.record(stream)
+        torch.cuda.nvtx.range_pop()
         barrier()
     ms = e0.elapsed_time(e1)
     gpu_launches = P.rtm_launch_count(h) - launches0 + args.steps  # + 1 a1 kernel per step

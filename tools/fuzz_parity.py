@@ -1,7 +1,8 @@
 """Randomised parity fuzz (GPU): random ragged shapes, velocities, initial conditions, sources
 and step counts; every kernel variant must equal the naive kernel bitwise and the fp32 oracle
-within the one-step tolerance scaled by the step count; slab decompositions (halo modes 0-2)
-must equal the single-slab result bitwise.  Usage: python tools/fuzz_parity.py [cases] [seed]"""
+within the one-step tolerance scaled by the step count (random z sweep direction, RTM_OPT_ZDIR);
+slab decompositions (halo modes 0-3, host-ordered or not, graphs or not) must equal the
+single-slab result bitwise.  Usage: python tools/fuzz_parity.py [cases] [seed]"""
 import sys
 import time
 from pathlib import Path
@@ -17,11 +18,15 @@ import rtm_inputs as ri  # noqa: E402
 C32 = ri.COEFFS_F32
 
 
-def run(v, steps, u0, up0, src, tile=None, devices=None, halo=0, tb_ctas=0, asyn=False):
+def run(v, steps, u0, up0, src, tile=None, devices=None, halo=0, tb_ctas=0, asyn=False, zdir=0,
+        host_ordered=0, graphs=1):
     nz, ny, nx = v.shape
     with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, devices=devices) as sim:
+        P.rtm_set_option(sim.h, P.RTM_OPT_ZDIR, zdir)
+        P.rtm_set_option(sim.h, P.RTM_OPT_GRAPHS, graphs)
         if halo:
             P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, halo)
+            P.rtm_set_option(sim.h, P.RTM_OPT_HOST_ORDERED, host_ordered)
         if tile is not None:
             sim.set_tile(tile)
         if tb_ctas:
@@ -81,11 +86,12 @@ def main():
         bad = []
         if err > 1e-5 * max(steps, 1) * 2:
             bad.append(f"naive vs oracle {err:.2e}")
+        zdir = int(rng.integers(0, 2))
         for t in range(1, ntiles):
-            out = run(v, steps, u0, up0, src, tile=t)
+            out = run(v, steps, u0, up0, src, tile=t, zdir=zdir)
             if not np.array_equal(out, base):
                 d = out != base
-                bad.append(f"{P.rtm_tile_name(t)}: {int(d.sum())} pts differ")
+                bad.append(f"{P.rtm_tile_name(t)} zdir={zdir}: {int(d.sum())} pts differ")
         tbs = [t for t in range(ntiles) if (P.rtm_tile_name(t) or "").startswith("tb2")]
         for t in tbs[:1]:  # multi-band two-step plans
             ctas = int(rng.integers(1, 13))
@@ -102,10 +108,12 @@ def main():
             bad.append(f"2 shots ({P.rtm_tile_name(t_sh)})")
         for G in (2, 3):
             if nz >= 10 * G:
-                for halo in (0, 1, 2):
-                    out = run(v, steps, u0, up0, src, devices=[0] * G, halo=halo)
+                for halo in (0, 1, 2, 3):
+                    ho, gr = int(rng.integers(0, 2)), int(rng.integers(0, 2))
+                    out = run(v, steps, u0, up0, src, devices=[0] * G, halo=halo, zdir=zdir,
+                              host_ordered=ho, graphs=gr)
                     if not np.array_equal(out, base):
-                        bad.append(f"slabs G={G} halo={halo}")
+                        bad.append(f"slabs G={G} halo={halo} host_ordered={ho} graphs={gr}")
         status = "OK" if not bad else "FAIL " + "; ".join(bad[:4])
         fails += bool(bad)
         print(f"case {c:3d} shape=({nz},{ny},{nx}) steps={steps} src={len(src)} oracle_err={err:.1e} {status}",
