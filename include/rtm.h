@@ -205,10 +205,12 @@ const char* rtm_tile_name(int tile_id);  /* e.g. "stream64x32k10d0"; NULL for un
  *   RTM_OPT_PDL        1: launch consecutive k_stream steps with programmatic dependent launch
  *                      (the next step's CTAs are scheduled while the previous grid drains and
  *                      wait on griddepcontrol.wait before touching memory); 0: plain launches.
- *   RTM_OPT_ZDIR       k_stream z sweep: 0 = every step sweeps z upward; 1 = odd-parity steps
- *                      sweep downward, so each step starts on the planes the previous step
- *                      touched last (they are still in L2).  Bitwise identical either way (the
- *                      z pair sums are commutative).
+ *   RTM_OPT_ZDIR       k_stream z sweep direction bits: 0 = every unit sweeps z upward; bit 0 =
+ *                      odd-parity steps sweep downward (each step starts on the planes the
+ *                      previous step touched last); bit 1 = every other unit (wave) of a
+ *                      persistent CTA sweeps downward (a wave starts where the previous one
+ *                      ended, next to the halo rows it shares with it).  Bitwise identical
+ *                      either way (the z pair sums are commutative).
  * Unknown key or out-of-range value -> RTM_EINVAL.  rtm_get_option returns -1 for unknown keys. */
 enum { RTM_OPT_ZCHUNK = 1, RTM_OPT_CACHE_MODE = 2, RTM_OPT_GRAPHS = 3, RTM_OPT_SHOT_ORDER = 4,
        RTM_OPT_HALO_MODE = 5, RTM_OPT_CHECK_EVERY = 6, RTM_OPT_TB_CTAS = 7, RTM_OPT_PDL = 8,

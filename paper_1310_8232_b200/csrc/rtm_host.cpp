@@ -162,7 +162,8 @@ struct rtm_ctx {
     int check_every = 0;    // NaN/Inf scan every k steps (0 = off)
     int tb_ctas = 0;        // two-step passes: max CTAs per band (0 = #SMs)
     bool pdl = false;       // programmatic dependent launch of consecutive k_stream steps
-    int zdir = 0;           // RTM_OPT_ZDIR: 1 = k_stream sweeps z downward on odd-parity steps
+    int zdir = 0;           // RTM_OPT_ZDIR bits: 1 = k_stream sweeps z downward on odd-parity
+                            // steps, 2 = on every other unit (wave) of a CTA
     int l2_bytes = 0;
     bool graphs = true;
     std::vector<HostSource> sources;
@@ -2197,7 +2198,7 @@ int rtm_set_option(rtm_ctx* c, int key, long long value) {
             c->host_ordered = value != 0;
             break;
         case RTM_OPT_ZDIR:
-            if (value < 0 || value > 1) return fail(RTM_EINVAL, "z direction mode %lld not in 0..1", value);
+            if (value < 0 || value > 3) return fail(RTM_EINVAL, "z direction mode %lld not in 0..3", value);
             c->zdir = (int)value;
             break;
         case RTM_OPT_HALO_MODE:

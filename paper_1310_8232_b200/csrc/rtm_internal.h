@@ -38,7 +38,7 @@ struct StencilParams {
     int r_chunks[2];           // z-chunks per range (tiled kernel work units)
     int tiles_x, tiles_y;      // tiled kernel: xy tiles
     int cache_mode;            // k_stream L2 policy knobs (see rtm_kernels.cu)
-    int zalt;                  // k_stream: sweep z downward on odd-parity steps (RTM_OPT_ZDIR)
+    int zalt;                  // k_stream: RTM_OPT_ZDIR bits (downward sweeps: odd steps / odd waves)
     int shot_major;            // 1: units ordered shot-slowest (each shot's tiles co-run);
                                // 0: shot-fastest (co-running CTAs share the C tile)
     // fused halo push (f1, in-process multi-slab): when non-null, owned planes [0,5) are also

@@ -368,6 +368,17 @@ __device__ __forceinline__ UnitGeom unit_geom(const StencilParams& p, int unit, 
     return g;
 }
 
+// z sweep direction of a unit (RTM_OPT_ZDIR bits): bit 0 — downward on odd-parity steps (a step
+// starts where the previous one ended); bit 1 — downward on every other unit of a CTA (wave w + 1
+// starts where wave w ended, so the halo rows its boxes share with wave w's tiles are still in
+// L2).  Every unit is computed identically either way (bitwise).
+__device__ __forceinline__ bool sweep_down(const StencilParams& p, int step_parity, int unit) {
+    int d = 0;
+    if (p.zalt & 1) d ^= step_parity & 1;
+    if (p.zalt & 2) d ^= ((unit - (int)blockIdx.x) / (int)gridDim.x) & 1;
+    return d != 0;
+}
+
 // Multi-step launches (MS): the unit index of (shot, chunk, tile) — the inverse of unit_geom.
 __device__ __forceinline__ int unit_index(const StencilParams& p, int shot, int chunk, int tile) {
     const int ntiles = p.tiles_x * p.tiles_y;
@@ -489,7 +500,7 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
                 // z sweep direction of this step (RTM_OPT_ZDIR): down on odd-parity steps, so a
                 // step starts on the planes the previous step touched last (still in L2).
                 // Buffer plane of sweep position j of the u box / of output i (u_prev tile):
-                const bool down = p.zalt && (((MS ? p.parity + k : p.parity) & 1) != 0);
+                const bool down = sweep_down(p, MS ? p.parity + k : p.parity, unit);
                 const int ub0 = (int)g.soff + (down ? g.ze + 9 : g.zs), ustep = down ? -1 : 1;
                 const int cz0 = down ? g.ze - 1 : g.zs;
                 auto put_u = [&](int j) {
@@ -577,7 +588,7 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
         // sweep direction (see the producer); the z register queue is filled in sweep order, so
         // a downward sweep mirrors it — the z pair sums u(z-m) + u(z+m) are commutative (IEEE
         // addition), so results are bitwise those of the upward sweep
-        const bool down = p.zalt && (((MS ? p.parity + k : p.parity) & 1) != 0);
+        const bool down = sweep_down(p, MS ? p.parity + k : p.parity, unit);
         const int z0 = down ? g.ze - 1 : g.zs, zstep = down ? -1 : 1;
         const long long pstep = down ? -p.plane : p.plane;
         float* outp = nextbuf + (g.soff + z0 + 5) * p.plane + col;  // also u_prev (D == 0)

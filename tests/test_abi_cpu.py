@@ -193,3 +193,28 @@ def test_blocksize_lattice_paper_worked_example(P):
     for bad in ((0, 5), (10, 1)):
         with pytest.raises(P.RtmError):
             P.rtm_blocksize_lattice(*bad)
+
+
+def test_peer_and_ipc_calls_validate_before_device(P):
+    """The NCCL-free slab bootstrap (peer contexts): NULL contexts and impossible slab requests
+    are rejected by the host code itself; without a GPU no peer context is created."""
+    with pytest.raises(P.RtmError) as e:
+        P.rtm_ipc_export(None)
+    assert e.value.code == P.RTM_EINVAL
+    with pytest.raises(P.RtmError) as e:
+        P.rtm_ipc_import(None, None, None)
+    assert e.value.code == P.RTM_EINVAL
+    with pytest.raises(ValueError):
+        P.rtm_ipc_import(None, b"short", None)
+    with pytest.raises(P.RtmError) as e:
+        P.rtm_set_host_barrier(None, lambda: None)
+    assert e.value.code == P.RTM_EINVAL
+    with pytest.raises(P.RtmError) as e:
+        P.rtm_get_dims(None)
+    assert e.value.code == P.RTM_EINVAL
+    assert P.rtm_last_enqueue_ms(None) == -1.0
+    for rank, world, nz in [(2, 2, 64), (0, 4, 30), (-1, 2, 64)]:  # rank out of range, thin slabs
+        with pytest.raises(P.RtmError) as e:
+            P.rtm_create_peer(16, 16, nz, 10.0, 1e-3, ri.COEFFS_F32, rank, world, 0)
+        assert e.value.code == P.RTM_EINVAL
+    assert P.RTM_IPC_RECORD_BYTES == 512

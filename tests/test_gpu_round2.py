@@ -315,11 +315,11 @@ def test_alternating_z_sweep_is_bitwise(P):
     ref, _ = _run_tile(P, v, [19], u0, up0, src, 35)
     ids = [t for t in range(1, P.rtm_num_tiles()) if (P.rtm_tile_name(t) or "").startswith(("stream", "ms"))]
     for t in ids:
-        for zc in (0, 7):
+        for zc, zd in ((0, 1), (7, 1), (7, 2), (5, 3)):
             with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32) as sim:
                 sim.set_tile(t)
                 P.rtm_set_zchunk(sim.h, zc)
-                P.rtm_set_option(sim.h, P.RTM_OPT_ZDIR, 1)
+                P.rtm_set_option(sim.h, P.RTM_OPT_ZDIR, zd)
                 sim.set_velocity(v)
                 for s in src:
                     sim.inject_source(*s)
@@ -327,7 +327,7 @@ def test_alternating_z_sweep_is_bitwise(P):
                 sim.step(1)
                 sim.step(18)
                 u, up = sim.read_fields()
-            assert np.array_equal(u, ref[0]) and np.array_equal(up, ref[1]), (P.rtm_tile_name(t), zc)
+            assert np.array_equal(u, ref[0]) and np.array_equal(up, ref[1]), (P.rtm_tile_name(t), zc, zd)
 
 
 @pytest.mark.parametrize("halo", [0, 1, 2, 3])
@@ -337,7 +337,7 @@ def test_alternating_z_sweep_with_slabs_is_bitwise(P, halo):
     nz, ny, nx = v.shape
     with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, devices=[0, 0, 0]) as sim:
         P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, halo)
-        P.rtm_set_option(sim.h, P.RTM_OPT_ZDIR, 1)
+        P.rtm_set_option(sim.h, P.RTM_OPT_ZDIR, 3)
         sim.set_velocity(v)
         for s in src:
             sim.inject_source(*s)
@@ -346,3 +346,53 @@ def test_alternating_z_sweep_with_slabs_is_bitwise(P, halo):
         sim.step(17)
         u, up = sim.read_fields()
     assert np.array_equal(u, ref_u) and np.array_equal(up, ref_up)
+
+
+# ----------------------------------------------------------------------------- peer-context errors
+def test_peer_context_contract(P):
+    """rtm_create_peer: world 1 behaves like a single-GPU context (bitwise); a rank with
+    neighbours refuses to step before its neighbours' records are imported, validates records
+    (magic, grid, world, rank, nzl) before opening anything, rejects halo mode 0 (no NCCL) and
+    fails collective calls without a rank barrier."""
+    v, u0, up0, src = _case(61, (30, 20, 32))
+    ref_u, _ = _single(P, v, 9, u0, up0, src)
+    nz, ny, nx = v.shape
+    h = P.rtm_create_peer(nx, ny, nz, 10.0, 1e-3, C32, 0, 1, 0)
+    try:
+        assert P.rtm_get_option(h, P.RTM_OPT_HALO_MODE) == 3
+        P.rtm_set_velocity(h, v)
+        for s in src:
+            P.rtm_inject_source(h, *s)
+        P.rtm_set_fields(h, u0, up0)
+        P.rtm_step(h, 9)
+        u = np.empty_like(u0)
+        P.rtm_read_field(h, u)
+        assert np.array_equal(u, ref_u)
+    finally:
+        P.rtm_destroy(h)
+    h0 = P.rtm_create_peer(nx, ny, nz, 10.0, 1e-3, C32, 0, 2, 0)
+    h1 = P.rtm_create_peer(nx + 4, ny, nz, 10.0, 1e-3, C32, 1, 2, 0)  # another grid
+    try:
+        assert P.rtm_get_dims(h0) == (nx, ny, 15, 1)
+        P.rtm_set_velocity(h0, v[:15])
+        with pytest.raises(P.RtmError) as e:
+            P.rtm_step(h0, 1)
+        assert e.value.code == P.RTM_ESTATE
+        with pytest.raises(P.RtmError) as e:   # rank 0 of 2 needs a hi record
+            P.rtm_ipc_import(h0, None, None)
+        assert e.value.code == P.RTM_EINVAL
+        with pytest.raises(P.RtmError) as e:
+            P.rtm_ipc_import(h0, None, bytes(512))
+        assert e.value.code == P.RTM_EINVAL and "not an RTM IPC record" in str(e.value)
+        with pytest.raises(P.RtmError) as e:   # rank 1's record, but of a different grid
+            P.rtm_ipc_import(h0, None, P.rtm_ipc_export(h1))
+        assert e.value.code == P.RTM_EINVAL and "grid" in str(e.value)
+        with pytest.raises(P.RtmError) as e:
+            P.rtm_set_option(h0, P.RTM_OPT_HALO_MODE, 0)
+        assert e.value.code == P.RTM_EINVAL
+        with pytest.raises(P.RtmError) as e:   # collective, no rank barrier installed
+            P.rtm_reset(h0)
+        assert e.value.code in (P.RTM_ESTATE, P.RTM_EINVAL)
+    finally:
+        P.rtm_destroy(h0)
+        P.rtm_destroy(h1)
