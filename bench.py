@@ -58,6 +58,10 @@ def parse():
                          "pull from CUDA-IPC mappings + flag protocol (SURVEY §8(e))")
     ap.add_argument("--pdl", type=int, default=-1, choices=[-1, 0, 1],
                     help="programmatic dependent launch of consecutive steps (-1: library default)")
+    ap.add_argument("--peer", action="store_true",
+                    help="N > 1 test mode: peer contexts (CUDA IPC, no NCCL) over a gloo group; "
+                         "ranks may share a GPU (then host-ordered) - exercises the N > 1 bench "
+                         "path on one GPU, not a scaling measurement")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="short run for ncu captures (no extras)")
@@ -148,7 +152,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ reference arm
-def bench_config(cfg, world, shots, halo, nsteps):
+def bench_config(cfg, world, shots, halo, nsteps, peer=False):
     """The `config` object of the JSON line — identical in both arms (workload only; the
     kernel variant the autotuner picks is reported outside it)."""
     nzl = cfg.nz // world if world > 1 else cfg.nz
@@ -157,7 +161,7 @@ def bench_config(cfg, world, shots, halo, nsteps):
             "sources": len(cfg.sources_xyz), "shots": shots,
             "parallelism": f"z-slab x{world}",
             "halo": ({0: "NCCL send/recv", 2: "fused IPC push + flags",
-                      3: "IPC copy-engine pull"}.get(halo)) if world > 1 else None,
+                      3: "IPC copy-engine pull"}.get(halo or (3 if peer else 0))) if world > 1 else None,
             "l2": "inputs larger than L2 (3 fields > 126 MB)"
             if cfg.nx * cfg.ny * nzl * shots * 4 > 126e6 else "L2-resident (no flush)"}
 
@@ -264,15 +268,26 @@ def main():
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    shared = args.peer and ndev < world  # test mode: several ranks per GPU
+    devi = local % ndev if args.peer else local
+    torch.cuda.set_device(devi)
+    dev = torch.device("cuda", devi)
     if world > 1:
-        tdist.init_process_group("nccl", device_id=dev)
+        if args.peer:
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=dev)
 
     cfg = ri.make_config(args.config, G=world if args.config == 5 else 1)
     nsteps = args.nsteps or cfg.steps
     v_full = cfg.velocity()
-    if world > 1:
+    if world > 1 and args.peer:
+        from paper_1310_8232_b200 import dist as pdist
+        z0, nzl = P.rtm_slab_range(cfg.nz, world, rank)
+        h = pdist.create_peer(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32, rank, world,
+                              devi, halo_mode=args.halo or 3, host_ordered=shared)
+    elif world > 1:
         z0, nzl = P.rtm_slab_range(cfg.nz, world, rank)
         uid = [P.rtm_get_unique_id() if rank == 0 else None]
         tdist.broadcast_object_list(uid, src=0)
@@ -332,7 +347,11 @@ def main():
 
     def barrier():
         if world > 1:
-            tdist.barrier(device_ids=[local])
+            if args.peer:
+                torch.cuda.synchronize(dev)
+                tdist.barrier()
+            else:
+                tdist.barrier(device_ids=[local])
         torch.cuda.synchronize(dev)
 
     def kernel_step():
@@ -344,7 +363,7 @@ def main():
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if args.peer else dev)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         return float(t.item())
 
@@ -468,7 +487,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
             "higher_is_better": True, "scaling": "strong" if cfg.k in (1, 2, 3, 4) else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, rtm_inputs)",
-            "config": bench_config(cfg, world, shots, args.halo, nsteps),
+            "config": bench_config(cfg, world, shots, args.halo, nsteps, args.peer),
             "kernel_variant": tile_name,
             "hbm_effective_gbs": round(value * bytes_per_pt, 1),
             "hbm_frac_of_8tbs": round(value * bytes_per_pt / 8000.0, 4),
@@ -499,7 +518,12 @@ def main():
             "autotune": tune,
             "cpu_baseline": cpu, "finite": finite,
         }
+        if args.peer:
+            line["test_mode"] = (f"peer contexts over gloo, {world} ranks on {min(ndev, world)} GPU(s)"
+                                 + (", host-ordered: not a scaling measurement" if shared else ""))
         print(json.dumps(line), flush=True)
+    if world > 1:
+        barrier()  # no rank unmaps or frees buffers a neighbour still reads
     P.rtm_destroy(h)
     if world > 1:
         tdist.destroy_process_group()

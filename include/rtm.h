@@ -205,7 +205,7 @@ const char* rtm_tile_name(int tile_id);  /* e.g. "stream64x32k10d0"; NULL for un
  *   RTM_OPT_PDL        1: launch consecutive k_stream steps with programmatic dependent launch
  *                      (the next step's CTAs are scheduled while the previous grid drains and
  *                      wait on griddepcontrol.wait before touching memory); 0: plain launches.
- *   RTM_OPT_ZDIR       k_stream z sweep direction bits: 0 = every unit sweeps z upward; bit 0 =
+ *   RTM_OPT_ZDIR       k_stream z sweep direction bits (default 2): 0 = every unit sweeps z upward; bit 0 =
  *                      odd-parity steps sweep downward (each step starts on the planes the
  *                      previous step touched last); bit 1 = every other unit (wave) of a
  *                      persistent CTA sweeps downward (a wave starts where the previous one

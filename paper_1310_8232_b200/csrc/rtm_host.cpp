@@ -162,7 +162,7 @@ struct rtm_ctx {
     int check_every = 0;    // NaN/Inf scan every k steps (0 = off)
     int tb_ctas = 0;        // two-step passes: max CTAs per band (0 = #SMs)
     bool pdl = false;       // programmatic dependent launch of consecutive k_stream steps
-    int zdir = 0;           // RTM_OPT_ZDIR bits: 1 = k_stream sweeps z downward on odd-parity
+    int zdir = 2;           // RTM_OPT_ZDIR bits: 1 = k_stream sweeps z downward on odd-parity
                             // steps, 2 = on every other unit (wave) of a CTA
     int l2_bytes = 0;
     bool graphs = true;

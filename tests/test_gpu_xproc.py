@@ -85,3 +85,24 @@ def test_peer_processes_on_one_gpu_bitwise_equal_single(P, reference, tmp_path, 
     assert np.array_equal(u, ref_u) and np.array_equal(up, ref_up)
     m = float(np.abs(orc).max())
     assert float(np.abs(u.astype(np.float64) - orc).max()) <= 1e-4 * m
+
+
+def test_bench_n2_path_with_peer_contexts_on_one_gpu():
+    """The N > 1 bench path (torchrun, slab ranges, collective reset / autotune, max-over-ranks
+    timing, e2e through the async host-buffer calls, one JSON line from rank 0) run as 2 ranks of
+    peer contexts on one GPU (`--peer`, host-ordered): a functional check of the line, not a
+    scaling number (the line says so in `test_mode`)."""
+    import json
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", OMP_NUM_THREADS="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           str(ROOT / "bench.py"), "--gpus", "2", "--peer", "--config", "1", "--steps", "2",
+           "--warmup", "3", "--no-cpu"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=str(ROOT))
+    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-5000:])
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and "test_mode" in d and d["finite"] is True
+    assert d["config"]["parallelism"] == "z-slab x2" and d["config"]["halo"] == "IPC copy-engine pull"
+    assert d["e2e"]["value"] > 0 and d["e2e"]["matches_device_result"] is True
