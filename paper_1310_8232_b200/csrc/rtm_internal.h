@@ -159,7 +159,6 @@ cudaError_t launch_tb2s(int id, const CUtensorMap tm[6], const TB2SParams& p, cu
 cudaError_t tb2s_variant_fn(int id, const void** fn, int* threads, size_t* smem);
 // after the last band of a pass: d_step[parity] += 2, ++*d_epoch
 cudaError_t launch_tb_advance(int* d_step, int parity, unsigned long long* d_epoch, cudaStream_t s);
-cudaError_t tb2s_variant_fn(int id, const void** fn, int* threads, size_t* smem);
 
 // a1: C = fp32((double(v)*dt/dx)^2), stats[0] = max(v) bits (v > 0), stats[1] = count of
 // invalid (non-finite or <= 0) velocities.  v and C may alias.
