@@ -1425,7 +1425,10 @@ int step_slabs(rtm_ctx* c, int nsteps) {
     int k = 0;
     while (k < nsteps) {
         const bool even = (c->step & 1) == 0;
-        if (c->graphs && !c->profiling && !c->slab_graphs_broken && even && nsteps - k >= 2 * GRAPH_PAIRS) {
+        // In-process slabs only: capturing NCCL send/recv (distributed contexts) is supported by
+        // NCCL but has never run on more than one GPU here, so those steps stay direct.
+        if (c->graphs && c->mode == 1 && !c->profiling && !c->slab_graphs_broken && even &&
+            nsteps - k >= 2 * GRAPH_PAIRS) {
             if (build_slab_graph(c) != RTM_OK) {
                 // e.g. a capture the driver refuses: direct launches from now on.  Events last
                 // recorded inside the aborted capture cannot be waited on: re-record them.
