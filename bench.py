@@ -326,8 +326,8 @@ def main():
         P.rtm_set_velocity_device(h, d_v.data_ptr())
         # two-step passes need a single-slab single-shot context and the resident kernel a
         # single slab; elsewhere they would run their paired k_stream variant.  The multi-step
-        # variants ("ms*") are left out: measured slower than single steps on C1-C4
-        # (profiles/sweep_r02_*.log)
+        # ("ms*") and two-row ("s2r*") variants are left out: measured slower than k_stream on
+        # C1-C5 (profiles/sweep_r02_*.log)
         kinds = ("stream",) + (("resident",) if world == 1 else ()) + \
             (("tb2",) if world == 1 and args.shots == 1 else ())
         cands = [t for t in range(P.rtm_num_tiles()) if (P.rtm_tile_name(t) or "").startswith(kinds)]

@@ -18,7 +18,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "librtm_b200.so"
-SOURCES = [CSRC / "rtm_kernels.cu", CSRC / "rtm_tb.cu", CSRC / "rtm_resident.cu", CSRC / "rtm_host.cpp"]
+SOURCES = [CSRC / "rtm_kernels.cu", CSRC / "rtm_tb.cu", CSRC / "rtm_resident.cu", CSRC / "rtm_stream2.cu",
+           CSRC / "rtm_host.cpp"]
 HEADERS = [CSRC / "rtm_internal.h", CSRC / "rtm_device.cuh", ROOT / "include" / "rtm.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -302,4 +302,52 @@ __device__ __forceinline__ void star4(const float* row, const float4 (&q)[N], fl
     star4_core<O>(q, yv, xs, upv, cv, c, out);
 }
 
+// ---- work units of the persistent streaming kernels (k_stream, k_stream2) ----------------
+struct UnitGeom {
+    int x0, y0, zs, ze;
+    int shot;
+    long long soff;  // buffer-plane offset of the shot: shot * (nzl + 10)
+};
+// unit = ((chunk * ntiles) + tile) * nshots + shot: shots fastest (concurrent CTAs share the
+// C tile through L2), then tiles (co-running xy neighbours share halos), then z-chunks.
+__device__ __forceinline__ UnitGeom unit_geom(const StencilParams& p, int unit, int TX, int TY) {
+    const int ntiles = p.tiles_x * p.tiles_y;
+    int shot;
+    if (p.shot_major) {
+        const int per_shot = ntiles * (p.r_chunks[0] + (p.nranges > 1 ? p.r_chunks[1] : 0));
+        shot = unit / per_shot;
+        unit -= shot * per_shot;
+    } else {
+        shot = unit % p.nshots;
+        unit /= p.nshots;
+    }
+    int chunk = unit / ntiles;
+    const int tile = unit - chunk * ntiles;
+    int r = 0;
+    if (chunk >= p.r_chunks[0]) {
+        r = 1;
+        chunk -= p.r_chunks[0];
+    }
+    UnitGeom g;
+    g.zs = p.r_begin[r] + static_cast<int>((long long)chunk * p.r_len[r] / p.r_chunks[r]);
+    g.ze = p.r_begin[r] + static_cast<int>((long long)(chunk + 1) * p.r_len[r] / p.r_chunks[r]);
+    const int tyi = tile / p.tiles_x;
+    g.x0 = (tile - tyi * p.tiles_x) * TX;
+    g.y0 = tyi * TY;
+    g.shot = shot;
+    g.soff = (long long)shot * (p.nzl + 10);
+    return g;
+}
+
+// z sweep direction of a unit (RTM_OPT_ZDIR bits): bit 0 — downward on odd-parity steps (a step
+// starts where the previous one ended); bit 1 — downward on every other unit of a CTA (wave w + 1
+// starts where wave w ended, so the halo rows its boxes share with wave w's tiles are still in
+// L2).  Every unit is computed identically either way (bitwise).
+__device__ __forceinline__ bool sweep_down(const StencilParams& p, int step_parity, int unit) {
+    int d = 0;
+    if (p.zalt & 1) d ^= step_parity & 1;
+    if (p.zalt & 2) d ^= ((unit - (int)blockIdx.x) / (int)gridDim.x) & 1;
+    return d != 0;
+}
+
 }  // namespace rtm

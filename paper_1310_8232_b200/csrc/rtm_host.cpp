@@ -383,7 +383,8 @@ int resolve_tile(const rtm_ctx* c) {
 // k_stream variant for odd remainders and for contexts it does not cover (slabs, shots).
 int single_variant(const rtm_ctx* c) {
     const int v = resolve_tile(c);
-    return variant(v).kind >= 3 ? variant(v).pair : v;
+    const int k = variant(v).kind;
+    return (k >= 3 && k != 7) ? variant(v).pair : v;
 }
 
 // 3D tensor map over a pitched device field: logical x extent nx (TMA zero-fills x >= nx, so
@@ -512,7 +513,7 @@ int launch_stencil(rtm_ctx* c, Slab& s, int parity, int b0, int l0, int b1, int 
         p.r_chunks[0] = choose_chunks(c, s.occupancy, nt * s.nshots, l0);  // units = tiles x chunks x shots
         p.r_chunks[1] = l1 > 0 ? choose_chunks(c, s.occupancy, nt * s.nshots, l1) : 0;
         CK(launch_variant(var, &s.tm_u[parity], &s.tm_in[parity ^ 1], &s.tm_c, p,
-                          c->num_sms * s.occupancy, st, c->pdl && variant(var).kind == 2));
+                          c->num_sms * s.occupancy, st, c->pdl && (variant(var).kind == 2 || variant(var).kind == 7)));
     }
     if (c->profiling) {
         CK(cudaEventRecord(e1, st));

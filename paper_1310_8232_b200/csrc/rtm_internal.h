@@ -65,7 +65,8 @@ struct TileVariant {
                                // warp), 4 k_tb2s (two time steps per HBM pass),
                                // 5 k_resident (many steps per launch, L2-resident grids),
                                // 6 k_stream multi-step (many steps per cooperative launch, units
-                               //   ordered by neighbour flags instead of launch boundaries)
+                               //   ordered by neighbour flags instead of launch boundaries),
+                               // 7 k_stream2 (two rows per consumer thread, rtm_stream2.cu)
     int TX, TY, K, D, MINB;    // tile (x, y), u ring depth, u_prev/C ring depth (0: LDG), min CTAs/SM
     int U;                     // z-loop unroll (register-queue rotation amortised over U planes)
     int KB, DB, L;             // kind 4: KB = W (store groups in flight before publication),
@@ -85,6 +86,16 @@ struct TileVariant {
     X(40, "resident256x2", 256, 2, 35)                    \
     X(41, "resident128x4", 128, 4, 35)                    \
     X(42, "resident512x1", 512, 1, 35)
+
+// Two-row streaming (kind 7, k_stream2 in rtm_stream2.cu) variants: X(id, name, TX, TY, K, D, MINB).
+// Warps per SM stay a multiple of 4 (8): the register file is split per SM sub-partition, so a
+// 9th warp would cap every thread at 168 registers and spill the two z queues.
+#define RTM_STREAM2_VARIANTS(X)                        \
+    X(51, "s2r64x28k10d6", 64, 28, 10, 6, 1)            \
+    X(52, "s2r128x14k8d4", 128, 14, 8, 4, 1)            \
+    X(53, "s2r64x12k10d6", 64, 12, 10, 6, 2)            \
+    X(54, "s2r128x6k8d5", 128, 6, 8, 5, 2)
+cudaError_t stream2_variant_fn(int id, const void** fn, int* threads, size_t* smem);
 
 // Variant table: index 0 is the naive kernel.
 int num_variants();

@@ -332,53 +332,6 @@ struct StreamShape {
     static_assert(TX % 4 == 0 && RS <= 256 && ROWS <= 256 && TX <= 256 && TY <= 256, "TMA box");
 };
 
-struct UnitGeom {
-    int x0, y0, zs, ze;
-    int shot;
-    long long soff;  // buffer-plane offset of the shot: shot * (nzl + 10)
-};
-// unit = ((chunk * ntiles) + tile) * nshots + shot: shots fastest (concurrent CTAs share the
-// C tile through L2), then tiles (co-running xy neighbours share halos), then z-chunks.
-__device__ __forceinline__ UnitGeom unit_geom(const StencilParams& p, int unit, int TX, int TY) {
-    const int ntiles = p.tiles_x * p.tiles_y;
-    int shot;
-    if (p.shot_major) {
-        const int per_shot = ntiles * (p.r_chunks[0] + (p.nranges > 1 ? p.r_chunks[1] : 0));
-        shot = unit / per_shot;
-        unit -= shot * per_shot;
-    } else {
-        shot = unit % p.nshots;
-        unit /= p.nshots;
-    }
-    int chunk = unit / ntiles;
-    const int tile = unit - chunk * ntiles;
-    int r = 0;
-    if (chunk >= p.r_chunks[0]) {
-        r = 1;
-        chunk -= p.r_chunks[0];
-    }
-    UnitGeom g;
-    g.zs = p.r_begin[r] + static_cast<int>((long long)chunk * p.r_len[r] / p.r_chunks[r]);
-    g.ze = p.r_begin[r] + static_cast<int>((long long)(chunk + 1) * p.r_len[r] / p.r_chunks[r]);
-    const int tyi = tile / p.tiles_x;
-    g.x0 = (tile - tyi * p.tiles_x) * TX;
-    g.y0 = tyi * TY;
-    g.shot = shot;
-    g.soff = (long long)shot * (p.nzl + 10);
-    return g;
-}
-
-// z sweep direction of a unit (RTM_OPT_ZDIR bits): bit 0 — downward on odd-parity steps (a step
-// starts where the previous one ended); bit 1 — downward on every other unit of a CTA (wave w + 1
-// starts where wave w ended, so the halo rows its boxes share with wave w's tiles are still in
-// L2).  Every unit is computed identically either way (bitwise).
-__device__ __forceinline__ bool sweep_down(const StencilParams& p, int step_parity, int unit) {
-    int d = 0;
-    if (p.zalt & 1) d ^= step_parity & 1;
-    if (p.zalt & 2) d ^= ((unit - (int)blockIdx.x) / (int)gridDim.x) & 1;
-    return d != 0;
-}
-
 // Multi-step launches (MS): the unit index of (shot, chunk, tile) — the inverse of unit_geom.
 __device__ __forceinline__ int unit_index(const StencilParams& p, int shot, int chunk, int tile) {
     const int ntiles = p.tiles_x * p.tiles_y;
@@ -830,6 +783,9 @@ static const TileVariant kVariants[] = {
     X(50, "ms64x30k10d6u11", 6, 64, 30, 10, 6, 1, 11, 48)
 #undef X2
 #undef X
+#define X(id, name, tx, ty, k, d, mb) {name, 7, tx, ty, k, d, mb, 11, 0, 0, 0, 0},
+    RTM_STREAM2_VARIANTS(X)
+#undef X
 };
 
 int num_variants() { return static_cast<int>(sizeof(kVariants) / sizeof(kVariants[0])); }
@@ -854,6 +810,7 @@ static cudaError_t prepare(const void** fn, int* threads, size_t* smem) {
 
 static cudaError_t variant_fn(int id, const void** fn, int* threads, size_t* smem) {
     if (id > 0 && id < num_variants() && variant(id).kind == 4) return tb2s_variant_fn(id, fn, threads, smem);
+    if (id > 0 && id < num_variants() && variant(id).kind == 7) return stream2_variant_fn(id, fn, threads, smem);
     if (id > 0 && id < num_variants() && variant(id).kind == 5) {
         *fn = nullptr;
         *threads = variant(id).TX;
@@ -913,7 +870,8 @@ cudaError_t launch_variant(int id, const CUtensorMap* tm_u, const CUtensorMap* t
     const void* fn;
     int threads;
     size_t smem;
-    if (variant(id).kind >= 3) return cudaErrorInvalidValue;  // two-step / multi-step: own launchers
+    const int kind = variant(id).kind;
+    if (kind >= 3 && kind != 7) return cudaErrorInvalidValue;  // two-step / resident / multi-step: own launchers
     cudaError_t e = variant_fn(id, &fn, &threads, &smem);
     if (e != cudaSuccess) return e;
     const long long units = (long long)p.tiles_x * p.tiles_y *
@@ -926,7 +884,7 @@ cudaError_t launch_variant(int id, const CUtensorMap* tm_u, const CUtensorMap* t
     const long long grid = units < max_ctas ? units : max_ctas;
     void* args[] = {const_cast<CUtensorMap*>(tm_u), const_cast<CUtensorMap*>(tm_up),
                     const_cast<CUtensorMap*>(tm_c), const_cast<StencilParams*>(&p),
-                    const_cast<CUtensorMap*>(tm_u), const_cast<CUtensorMap*>(tm_up)};
+                    const_cast<CUtensorMap*>(tm_u), const_cast<CUtensorMap*>(tm_up)};  // k_stream2 reads the first 4
     if (!pdl) return cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(threads), args, smem, s);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(grid));

@@ -102,7 +102,7 @@ def test_halo_plan_layout(P):
 def test_tile_table(P):
     n = P.rtm_num_tiles()
     assert n >= 2 and P.rtm_tile_name(0) == "naive"
-    assert all(P.rtm_tile_name(i).startswith(("tma", "stream", "tb2", "resident", "ms")) for i in range(1, n))
+    assert all(P.rtm_tile_name(i).startswith(("tma", "stream", "tb2", "resident", "ms", "s2r")) for i in range(1, n))
     assert P.rtm_tile_name(n) is None and P.rtm_tile_name(-5) is None
 
 

@@ -313,7 +313,7 @@ def test_alternating_z_sweep_is_bitwise(P):
     src = [(0, 0, 0, w), (75, 44, 40, -w), (33, 20, 13, w), (34, 21, 27, 0.5 * w)]
     nz, ny, nx = shape
     ref, _ = _run_tile(P, v, [19], u0, up0, src, 35)
-    ids = [t for t in range(1, P.rtm_num_tiles()) if (P.rtm_tile_name(t) or "").startswith(("stream", "ms"))]
+    ids = [t for t in range(1, P.rtm_num_tiles()) if (P.rtm_tile_name(t) or "").startswith(("stream", "ms", "s2r"))]
     for t in ids:
         for zc, zd in ((0, 1), (7, 1), (7, 2), (5, 3)):
             with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32) as sim:
