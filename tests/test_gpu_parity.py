@@ -222,7 +222,7 @@ def test_multislab_on_one_gpu_bitwise_equals_single(P, G, halo):
     assert relerr(got, orc) <= TOL_1 * 10
 
 
-@pytest.mark.parametrize("halo", [0, 2])
+@pytest.mark.parametrize("halo", [0, 2, 3])
 def test_dist_world1_equals_single(P, halo):
     """The NCCL-communicator context at world 1; halo mode 2 runs its collective set-up (IPC
     handle export + NCCL all-gather) and the flag-protocol step path."""

@@ -396,3 +396,26 @@ def test_peer_context_contract(P):
     finally:
         P.rtm_destroy(h0)
         P.rtm_destroy(h1)
+
+
+def test_autotune_in_pull_mode_and_host_ordered_in_process(P):
+    """Halo mode 3 in-process through the collective restarts: autotune (new flag generation),
+    reset, resume; host-ordered stepping interleaved with device-ordered stepping."""
+    v, u0, up0, src = _case(123, (60, 33, 72))
+    ref_u, ref_up = _single(P, v, 26, u0, up0, src)
+    nz, ny, nx = v.shape
+    with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, devices=[0, 0, 0, 0]) as sim:
+        P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, 3)
+        sim.set_velocity(v)
+        for s in src:
+            sim.inject_source(*s)
+        sim.set_fields(u0, up0)
+        sim.step(4)
+        P.rtm_autotune(sim.h, 3, tiles=[35, 10, 1], zchunks=[0, 0, 5])
+        sim.step(7)
+        P.rtm_set_option(sim.h, P.RTM_OPT_HOST_ORDERED, 1)
+        sim.step(6)
+        P.rtm_set_option(sim.h, P.RTM_OPT_HOST_ORDERED, 0)
+        sim.step(9)
+        u, up = sim.read_fields()
+    assert np.array_equal(u, ref_u) and np.array_equal(up, ref_up)
