@@ -326,9 +326,10 @@ def main():
         P.rtm_set_velocity_device(h, d_v.data_ptr())
         # two-step passes need a single-slab single-shot context and the resident kernel a
         # single slab; elsewhere they would run their paired k_stream variant.  The multi-step
-        # ("ms*") and two-row ("s2r*") variants are left out: measured slower than k_stream on
-        # C1-C5 (profiles/sweep_r02_*.log)
-        kinds = ("stream",) + (("resident",) if world == 1 else ()) + \
+        # variants ("ms*") are left out (measured slower on C1-C5); the two-row
+        # variants ("s2r*", fewer instructions per point) stay in: on a power-capped box the
+        # lower-instruction variants can win (the tuner measures on the box it runs on)
+        kinds = ("stream", "s2r") + (("resident",) if world == 1 else ()) + \
             (("tb2",) if world == 1 and args.shots == 1 else ())
         cands = [t for t in range(P.rtm_num_tiles()) if (P.rtm_tile_name(t) or "").startswith(kinds)]
         zcs = None
