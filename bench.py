@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--tile", type=int, default=-1,
                     help="kernel variant; -1 = choose with rtm_autotune (untimed, before warm-up)")
-    ap.add_argument("--tune-ni", type=int, default=8, help="autotune iterations per candidate")
+    ap.add_argument("--tune-ni", type=int, default=12,
+                    help="autotune iterations per candidate (raised automatically on small grids)")
     ap.add_argument("--lattice", type=int, default=0,
                     help="P > 1: autotune over the stream tiles x the paper's P-parts z-chunk "
                          "lattice (PAPER.md:296-301); 0: automatic z-chunk per tile")

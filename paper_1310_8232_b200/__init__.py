@@ -44,7 +44,7 @@ class Simulation:
         return (self.nzl, self.ny, self.nx)
 
     def set_velocity(self, v):
-        _r.rtm_set_velocity(self.h, v, n=self.nx * self.ny * self.nzl)
+        _r.rtm_set_velocity(self.h, v)
 
     def inject_source(self, ix, iy, iz, samples, shot=0):
         _r.rtm_inject_source_shot(self.h, shot, ix, iy, iz, samples)

@@ -176,7 +176,7 @@ def rtm_create(nx, ny, nz, dx, dt, coeffs):
     return h
 
 
-def rtm_set_velocity(h, v, n=None):
+def rtm_set_velocity(h, v):
     v = _f32(v, _n_velocity(h), "v")
     return _check(lib.rtm_set_velocity(h, _ptr(v)))
 

@@ -218,3 +218,29 @@ def test_peer_and_ipc_calls_validate_before_device(P):
             P.rtm_create_peer(16, 16, nz, 10.0, 1e-3, ri.COEFFS_F32, rank, world, 0)
         assert e.value.code == P.RTM_EINVAL
     assert P.RTM_IPC_RECORD_BYTES == 512
+
+
+def _build_c_example(tmp_path):
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if not cc:
+        pytest.skip("no C compiler")
+    lib_dir = ROOT / "paper_1310_8232_b200"
+    exe = tmp_path / "rtm_c1"
+    subprocess.run([cc, "-O2", "-Wall", "-Werror", "-I", str(ROOT / "include"),
+                    str(ROOT / "examples" / "rtm_c1.c"), "-L", str(lib_dir), "-lrtm_b200",
+                    f"-Wl,-rpath,{lib_dir}", "-lm", "-o", str(exe)], check=True)
+    return exe
+
+
+def test_c_example_builds_against_the_header_and_library(P, tmp_path):
+    """examples/rtm_c1.c uses the C ABI from plain C (no Python): it compiles with -Wall -Werror
+    against include/rtm.h, links librtm_b200.so, and without a GPU fails loudly (no fallback)."""
+    import subprocess
+    import torch
+    exe = _build_c_example(tmp_path)
+    if torch.cuda.is_available():
+        pytest.skip("GPU present (tests/test_gpu_round2.py runs it)")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 1 and "no CUDA device" in r.stderr

@@ -419,3 +419,22 @@ def test_autotune_in_pull_mode_and_host_ordered_in_process(P):
         sim.step(9)
         u, up = sim.read_fields()
     assert np.array_equal(u, ref_u) and np.array_equal(up, ref_up)
+
+
+def test_c_example_matches_the_oracle(P, tmp_path):
+    """examples/rtm_c1.c (plain C through include/rtm.h) runs C1 on the GPU; its max|u| equals
+    the fp32 oracle's within the north-star tolerance."""
+    import re
+    import subprocess
+    import sys
+    sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parent))
+    from test_abi_cpu import _build_c_example
+    import oracle
+    exe = _build_c_example(tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    m = float(re.search(r"max\|u\| = ([0-9.eE+-]+)", r.stdout).group(1))
+    cfg = ri.make_config(1)
+    ref = oracle.run(cfg.velocity(), cfg.dx, cfg.dt, C32, cfg.steps, sources=cfg.sources())
+    mref = float(np.abs(ref).max())
+    assert abs(m - mref) <= 1e-4 * mref, (m, mref)
