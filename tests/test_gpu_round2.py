@@ -438,3 +438,25 @@ def test_c_example_matches_the_oracle(P, tmp_path):
     ref = oracle.run(cfg.velocity(), cfg.dx, cfg.dt, C32, cfg.steps, sources=cfg.sources())
     mref = float(np.abs(ref).max())
     assert abs(m - mref) <= 1e-4 * mref, (m, mref)
+
+
+@pytest.mark.parametrize("halo", [0, 1, 2, 3])
+def test_two_row_and_u11_variants_in_slab_modes(P, halo):
+    """The tuner may pick a two-row (k_stream2) or U = 11 variant for a slab context: boundary
+    2-range launches (modes 0, 3) and epilogue pushes (modes 1, 2) stay bitwise equal to G = 1."""
+    v, u0, up0, src = _case(202, (50, 30, 68))
+    ref_u, ref_up = _single(P, v, 13, u0, up0, src)
+    nz, ny, nx = v.shape
+    ids = [t for t in range(1, P.rtm_num_tiles())
+           if (P.rtm_tile_name(t) or "").startswith("s2r") or (P.rtm_tile_name(t) or "").endswith("u11")]
+    for t in ids:
+        with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, devices=[0, 0, 0]) as sim:
+            sim.set_tile(t)
+            P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, halo)
+            sim.set_velocity(v)
+            for s in src:
+                sim.inject_source(*s)
+            sim.set_fields(u0, up0)
+            sim.step(13)
+            u, up = sim.read_fields()
+        assert np.array_equal(u, ref_u) and np.array_equal(up, ref_up), P.rtm_tile_name(t)
