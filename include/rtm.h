@@ -211,10 +211,14 @@ const char* rtm_tile_name(int tile_id);  /* e.g. "stream64x32k10d0"; NULL for un
  *                      persistent CTA sweeps downward (a wave starts where the previous one
  *                      ended, next to the halo rows it shares with it).  Bitwise identical
  *                      either way (the z pair sums are commutative).
+ *   RTM_OPT_SLAB_SHARE 1: slabs of an in-process context that share a device (one-GPU decomposition
+ *                      runs, devices = [0, 0, ...]) split its SMs — each slab's persistent grid
+ *                      gets #SMs × occupancy / (slabs on the device) CTAs — so their kernels can run
+ *                      concurrently; 0 (default): every launch gets all SMs.
  * Unknown key or out-of-range value -> RTM_EINVAL.  rtm_get_option returns -1 for unknown keys. */
 enum { RTM_OPT_ZCHUNK = 1, RTM_OPT_CACHE_MODE = 2, RTM_OPT_GRAPHS = 3, RTM_OPT_SHOT_ORDER = 4,
        RTM_OPT_HALO_MODE = 5, RTM_OPT_CHECK_EVERY = 6, RTM_OPT_TB_CTAS = 7, RTM_OPT_PDL = 8,
-       RTM_OPT_HOST_ORDERED = 9, RTM_OPT_ZDIR = 10 };
+       RTM_OPT_HOST_ORDERED = 9, RTM_OPT_ZDIR = 10, RTM_OPT_SLAB_SHARE = 11 };
 int rtm_set_option(rtm_ctx* ctx, int key, long long value);
 long long rtm_get_option(rtm_ctx* ctx, int key);
 

@@ -79,6 +79,7 @@ struct Slab {
     int dev = 0;
     int z0 = 0, nzl = 0;
     int nshots = 1;                      // batched independent wavefields sharing C
+    int share = 1;                       // slabs of this context on the same device
     bool lo_nb = false, hi_nb = false;
     float* buf[2] = {nullptr, nullptr};  // nshots*(nzl+10) planes each
     size_t buf_planes() const { return (size_t)nshots * (nzl + 10); }
@@ -162,6 +163,7 @@ struct rtm_ctx {
     int check_every = 0;    // NaN/Inf scan every k steps (0 = off)
     int tb_ctas = 0;        // two-step passes: max CTAs per band (0 = #SMs)
     bool pdl = false;       // programmatic dependent launch of consecutive k_stream steps
+    bool share_sms = false; // RTM_OPT_SLAB_SHARE: slabs sharing a device split its SMs
     int zdir = 2;           // RTM_OPT_ZDIR bits: 1 = k_stream sweeps z downward on odd-parity
                             // steps, 2 = on every other unit (wave) of a CTA
     int l2_bytes = 0;
@@ -430,10 +432,10 @@ int ensure_tmaps(rtm_ctx* c, Slab& s, int var) {
 }
 
 // z-chunks for a range of len planes: minimise (wave quantisation) x (chunk-halo re-read).
-int choose_chunks(const rtm_ctx* c, int occ, int ntiles, int len) {
+int choose_chunks(const rtm_ctx* c, int occ, int ntiles, int len, int share = 1) {
     if (c->zchunk > 0) return std::max(1, (len + c->zchunk - 1) / c->zchunk);
     if (occ < 1) occ = 1;
-    const double S = (double)c->num_sms * occ;
+    const double S = std::max(1.0, (double)c->num_sms * occ / share);
     int best = 1;
     double bestc = 1e300;
     const int maxc = std::max(1, len / 8);
@@ -510,10 +512,14 @@ int launch_stencil(rtm_ctx* c, Slab& s, int parity, int b0, int l0, int b1, int 
         p.tiles_x = (c->nx + tv.TX - 1) / tv.TX;
         p.tiles_y = (c->ny + tv.TY - 1) / tv.TY;
         const int nt = p.tiles_x * p.tiles_y;
-        p.r_chunks[0] = choose_chunks(c, s.occupancy, nt * s.nshots, l0);  // units = tiles x chunks x shots
-        p.r_chunks[1] = l1 > 0 ? choose_chunks(c, s.occupancy, nt * s.nshots, l1) : 0;
+        // slabs that share a device (one-GPU decomposition runs) may split its SMs so that all of
+        // them run concurrently (RTM_OPT_SLAB_SHARE); otherwise every launch gets all SMs
+        const int share = c->share_sms ? s.share : 1;
+        p.r_chunks[0] = choose_chunks(c, s.occupancy, nt * s.nshots, l0, share);  // units = tiles x chunks x shots
+        p.r_chunks[1] = l1 > 0 ? choose_chunks(c, s.occupancy, nt * s.nshots, l1, share) : 0;
         CK(launch_variant(var, &s.tm_u[parity], &s.tm_in[parity ^ 1], &s.tm_c, p,
-                          c->num_sms * s.occupancy, st, c->pdl && (variant(var).kind == 2 || variant(var).kind == 7)));
+                          std::max(1, c->num_sms * s.occupancy / share), st,
+                          c->pdl && (variant(var).kind == 2 || variant(var).kind == 7)));
     }
     if (c->profiling) {
         CK(cudaEventRecord(e1, st));
@@ -1787,6 +1793,9 @@ rtm_ctx* rtm_create_multi(int nx, int ny, int nz, float dx, float dt, const floa
         s.hi_nb = r < nslabs - 1;
         c->slabs.push_back(s);
     }
+    for (int r = 0; r < nslabs; ++r)
+        for (int q = 0; q < nslabs; ++q)
+            if (devices[q] == devices[r] && q != r) ++c->slabs[r].share;
     for (int r = 0; r < nslabs; ++r)  // best effort peer access (copies work either way)
         for (int q = 0; q < nslabs; ++q)
             if (devices[r] != devices[q]) {
@@ -2201,6 +2210,10 @@ int rtm_set_option(rtm_ctx* c, int key, long long value) {
             if (value < 0 || value > 1) return fail(RTM_EINVAL, "host ordered %lld not in 0..1", value);
             c->host_ordered = value != 0;
             break;
+        case RTM_OPT_SLAB_SHARE:
+            if (value < 0 || value > 1) return fail(RTM_EINVAL, "slab share %lld not in 0..1", value);
+            c->share_sms = value != 0;
+            break;
         case RTM_OPT_ZDIR:
             if (value < 0 || value > 3) return fail(RTM_EINVAL, "z direction mode %lld not in 0..3", value);
             c->zdir = (int)value;
@@ -2252,6 +2265,7 @@ long long rtm_get_option(rtm_ctx* c, int key) {
         case RTM_OPT_PDL: return c->pdl ? 1 : 0;
         case RTM_OPT_HOST_ORDERED: return c->host_ordered ? 1 : 0;
         case RTM_OPT_ZDIR: return c->zdir;
+        case RTM_OPT_SLAB_SHARE: return c->share_sms ? 1 : 0;
         default: return -1;
     }
 }

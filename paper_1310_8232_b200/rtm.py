@@ -24,6 +24,7 @@ RTM_OPT_TB_CTAS = 7
 RTM_OPT_PDL = 8
 RTM_OPT_HOST_ORDERED = 9
 RTM_OPT_ZDIR = 10
+RTM_OPT_SLAB_SHARE = 11
 RTM_IPC_RECORD_BYTES = 512
 _NAMES = {0: "RTM_OK", -1: "RTM_EINVAL", -2: "RTM_ECFL", -3: "RTM_ENOMEM", -4: "RTM_ECUDA",
           -5: "RTM_ENCCL", -6: "RTM_ESTATE", -7: "RTM_EUNSTABLE"}

@@ -460,3 +460,24 @@ def test_two_row_and_u11_variants_in_slab_modes(P, halo):
             sim.step(13)
             u, up = sim.read_fields()
         assert np.array_equal(u, ref_u) and np.array_equal(up, ref_up), P.rtm_tile_name(t)
+
+
+@pytest.mark.parametrize("halo", [0, 1, 2, 3])
+def test_slab_share_bitwise(P, halo):
+    """RTM_OPT_SLAB_SHARE: slabs sharing a device split its SMs (smaller persistent grids,
+    z-chunks chosen for the share) — bitwise equal to G = 1, with and without graphs."""
+    v, u0, up0, src = _case(303, (64, 33, 72))
+    ref_u, ref_up = _single(P, v, 37, u0, up0, src)
+    nz, ny, nx = v.shape
+    for graphs in (0, 1):
+        with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32, devices=[0] * 4) as sim:
+            P.rtm_set_option(sim.h, P.RTM_OPT_HALO_MODE, halo)
+            P.rtm_set_option(sim.h, P.RTM_OPT_SLAB_SHARE, 1)
+            P.rtm_set_option(sim.h, P.RTM_OPT_GRAPHS, graphs)
+            sim.set_velocity(v)
+            for s in src:
+                sim.inject_source(*s)
+            sim.set_fields(u0, up0)
+            sim.step(37)
+            u, up = sim.read_fields()
+        assert np.array_equal(u, ref_u) and np.array_equal(up, ref_up), graphs

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--slabs", type=int, default=1, help="in-process z-slabs (all on visible GPUs round-robin)")
     ap.add_argument("--halo", type=int, default=0, help="RTM_OPT_HALO_MODE for --slabs > 1")
     ap.add_argument("--graphs", type=int, default=1, help="RTM_OPT_GRAPHS (CUDA-graph replays)")
+    ap.add_argument("--share", type=int, default=0, help="RTM_OPT_SLAB_SHARE for --slabs > 1")
     ap.add_argument("--pdl", default="0", help="comma list of RTM_OPT_PDL values (interleaved)")
     ap.add_argument("--zdir", default="0", help="comma list of RTM_OPT_ZDIR values (interleaved)")
     args = ap.parse_args()
@@ -39,6 +40,7 @@ def main():
         h = P.rtm_create_multi(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32,
                                [k % ndev for k in range(args.slabs)])
         P.rtm_set_option(h, P.RTM_OPT_HALO_MODE, args.halo)
+        P.rtm_set_option(h, P.RTM_OPT_SLAB_SHARE, args.share)
     elif args.shots > 1:
         h = P.rtm_create_batch(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32, args.shots)
     else:
@@ -79,7 +81,7 @@ def main():
             gpts = cfg.points * args.shots / ms / 1e6
             r = {"tile": t, "name": P.rtm_tile_name(t), "zchunk": zc, "shot_order": so, "pdl": pdl,
                  "zdir": zd,
-                 "slabs": args.slabs, "halo": args.halo, "graphs": args.graphs,
+                 "slabs": args.slabs, "halo": args.halo, "graphs": args.graphs, "share": args.share,
                  "enqueue_ms_per_step": round(P.rtm_last_enqueue_ms(h) / args.ni, 4),
                  "cache": hex(P.rtm_get_option(h, P.RTM_OPT_CACHE_MODE)), "ms_per_step": round(ms, 4),
                  "gpts": round(gpts, 2), "eff_gbs": round(16 * gpts, 1)}
