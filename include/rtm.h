@@ -209,7 +209,9 @@ const char* rtm_tile_name(int tile_id);  /* e.g. "stream64x32k10d0"; NULL for un
  *                      odd-parity steps sweep downward (each step starts on the planes the
  *                      previous step touched last); bit 1 = every other unit (wave) of a
  *                      persistent CTA sweeps downward (a wave starts where the previous one
- *                      ended, next to the halo rows it shares with it).  Bitwise identical
+ *                      ended, next to the halo rows it shares with it); bit 2 = odd z-chunks
+ *                      sweep downward (neighbouring chunks start / end on the planes they share,
+ *                      so each z-halo plane is read by both at the same time).  Bitwise identical
  *                      either way (the z pair sums are commutative).
  *   RTM_OPT_SLAB_SHARE 1: slabs of an in-process context that share a device (one-GPU decomposition
  *                      runs, devices = [0, 0, ...]) split its SMs — each slab's persistent grid

@@ -347,6 +347,13 @@ __device__ __forceinline__ bool sweep_down(const StencilParams& p, int step_pari
     int d = 0;
     if (p.zalt & 1) d ^= step_parity & 1;
     if (p.zalt & 2) d ^= ((unit - (int)blockIdx.x) / (int)gridDim.x) & 1;
+    if (p.zalt & 4) {  // odd z-chunks sweep downward: neighbouring chunks start and end on the
+                       // planes they share, so each z-halo plane is read by both at the same time
+        const int ntiles = p.tiles_x * p.tiles_y;
+        const int per_shot = ntiles * (p.r_chunks[0] + (p.nranges > 1 ? p.r_chunks[1] : 0));
+        const int u = p.shot_major ? unit % per_shot : unit / p.nshots;
+        d ^= (u / ntiles) & 1;
+    }
     return d != 0;
 }
 

@@ -2215,7 +2215,7 @@ int rtm_set_option(rtm_ctx* c, int key, long long value) {
             c->share_sms = value != 0;
             break;
         case RTM_OPT_ZDIR:
-            if (value < 0 || value > 3) return fail(RTM_EINVAL, "z direction mode %lld not in 0..3", value);
+            if (value < 0 || value > 7) return fail(RTM_EINVAL, "z direction mode %lld not in 0..7", value);
             c->zdir = (int)value;
             break;
         case RTM_OPT_HALO_MODE:

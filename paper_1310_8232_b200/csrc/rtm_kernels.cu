@@ -356,25 +356,30 @@ __device__ __noinline__ void wait_unit_flags(const StencilParams& p, int unit, u
     }
     const int chunk = rest / ntiles, tile = rest - chunk * ntiles;
     const int ty = tile / p.tiles_x, tx = tile - ty * p.tiles_x;
-    int nb[7];
-    int m = 0;
-    nb[m++] = unit;
-    if (tx > 0) nb[m++] = unit_index(p, shot, chunk, tile - 1);
-    if (tx + 1 < p.tiles_x) nb[m++] = unit_index(p, shot, chunk, tile + 1);
-    if (ty > 0) nb[m++] = unit_index(p, shot, chunk, tile - p.tiles_x);
-    if (ty + 1 < p.tiles_y) nb[m++] = unit_index(p, shot, chunk, tile + p.tiles_x);
-    if (chunk > 0) nb[m++] = unit_index(p, shot, chunk - 1, tile);
-    if (chunk + 1 < p.r_chunks[0]) nb[m++] = unit_index(p, shot, chunk + 1, tile);
-    for (int i = 0; i < m; ++i) {
-        const unsigned long long* f = p.flags + nb[i];
-        if (ld_acquire_gpu_u64(f) >= target) continue;
-        const unsigned long long t0 = globaltimer_ns();
+    // chunk c covers planes [zb(c), zb(c+1)); its u boxes read planes [zb(c) - 5, zb(c+1) + 5), so
+    // every chunk of the same tile that intersects that range is a z-neighbour (more than one on
+    // each side when chunks are shorter than the 5-plane halo)
+    auto zb = [&](int c2) {
+        return p.r_begin[0] + static_cast<int>((long long)c2 * p.r_len[0] / p.r_chunks[0]);
+    };
+    const int lo = zb(chunk) - RADIUS, hi = zb(chunk + 1) + RADIUS;
+    auto check = [&](int v, unsigned long long t0) {
+        const unsigned long long* f = p.flags + v;
+        if (ld_acquire_gpu_u64(f) >= target) return;
         unsigned spins = 0;
         while (ld_acquire_gpu_u64(f) < target) {
             __nanosleep(64);
             if ((++spins & 255) == 0 && globaltimer_ns() - t0 > kWatchdogNs) __trap();
         }
-    }
+    };
+    const unsigned long long t0 = globaltimer_ns();
+    check(unit, t0);
+    if (tx > 0) check(unit_index(p, shot, chunk, tile - 1), t0);
+    if (tx + 1 < p.tiles_x) check(unit_index(p, shot, chunk, tile + 1), t0);
+    if (ty > 0) check(unit_index(p, shot, chunk, tile - p.tiles_x), t0);
+    if (ty + 1 < p.tiles_y) check(unit_index(p, shot, chunk, tile + p.tiles_x), t0);
+    for (int c2 = chunk - 1; c2 >= 0 && zb(c2 + 1) > lo; --c2) check(unit_index(p, shot, c2, tile), t0);
+    for (int c2 = chunk + 1; c2 < p.r_chunks[0] && zb(c2) < hi; ++c2) check(unit_index(p, shot, c2, tile), t0);
     fence_proxy_async_global();
 }
 
@@ -691,13 +696,12 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
         gu += n + 10;
         gc += n;
         if constexpr (MS) {
-            // publish "unit done with step k": every consumer warp's stores of the unit, then a
-            // gpu-scope release (cumulative over the CTA barrier) read by the neighbours' producers
+            // publish "unit done with step k": every consumer thread orders its own stores of the
+            // unit at gpu scope (fence), the CTA barrier collects them, one gpu-scope release is
+            // read by the neighbours' producers (acquire + async-proxy fence before their TMA)
+            __threadfence();
             asm volatile("bar.sync 1, %0;" ::"n"(S::NW * 32) : "memory");
-            if (tid == 0) {
-                __threadfence();
-                st_release_gpu_u64(p.flags + unit, p.epoch | (unsigned long long)(k + 1));
-            }
+            if (tid == 0) st_release_gpu_u64(p.flags + unit, p.epoch | (unsigned long long)(k + 1));
         }
     }
 }

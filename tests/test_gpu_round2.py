@@ -315,7 +315,7 @@ def test_alternating_z_sweep_is_bitwise(P):
     ref, _ = _run_tile(P, v, [19], u0, up0, src, 35)
     ids = [t for t in range(1, P.rtm_num_tiles()) if (P.rtm_tile_name(t) or "").startswith(("stream", "ms", "s2r"))]
     for t in ids:
-        for zc, zd in ((0, 1), (7, 1), (7, 2), (5, 3)):
+        for zc, zd in ((0, 1), (7, 1), (7, 2), (5, 3), (6, 4), (5, 6)):
             with P.Simulation(nx, ny, nz, 10.0, 1e-3, C32) as sim:
                 sim.set_tile(t)
                 P.rtm_set_zchunk(sim.h, zc)
@@ -481,3 +481,23 @@ def test_slab_share_bitwise(P, halo):
             sim.step(37)
             u, up = sim.read_fields()
         assert np.array_equal(u, ref_u) and np.array_equal(up, ref_up), graphs
+
+
+@pytest.mark.parametrize("zchunk", [2, 3, 5])
+def test_multistep_chunks_shorter_than_the_halo(P, zchunk):
+    """Multi-step launches with z-chunks shorter than the 5-plane halo: a unit's boxes then reach
+    two or more chunks up and down, all of which must have published the previous step.  (A round-2
+    stress run found the kernel waiting only for chunks c±1: 517 of 2304 runs differed; the wait now
+    covers every chunk the halo intersects — `profiles/ms_stress_r02.log`.)"""
+    rng = np.random.default_rng(31 + zchunk)
+    shape = (46, 57, 55)
+    v = rng.uniform(1500, 4300, shape).astype(np.float32)
+    u0, up0 = ri.random_fields(shape, seed=zchunk)
+    w = ri.source_samples(3000.0, 1e-3, 15.0, 40)
+    nz, ny, nx = shape
+    src = [(0, 0, 0, w), (nx - 1, ny - 1, nz - 1, -w), (nx // 2, ny // 3, nz // 2, w)]
+    ref, _ = _run_tile(P, v, [23], u0, up0, src, 35)
+    for t in _ms_ids(P):
+        for rep in range(3):
+            got, _ = _run_tile(P, v, [1, 22], u0, up0, src, t, zchunk=zchunk)
+            assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1]), (P.rtm_tile_name(t), rep)

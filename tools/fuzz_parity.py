@@ -86,7 +86,7 @@ def main():
         bad = []
         if err > 1e-5 * max(steps, 1) * 2:
             bad.append(f"naive vs oracle {err:.2e}")
-        zdir = int(rng.integers(0, 4))
+        zdir = int(rng.integers(0, 8))
         for t in range(1, ntiles):
             out = run(v, steps, u0, up0, src, tile=t, zdir=zdir)
             if not np.array_equal(out, base):
