@@ -24,6 +24,14 @@
 #include <cstdio>
 #include <type_traits>
 
+// 1 (default): single-step k_stream reads the 5 leading z-halo planes of a unit (only the z
+// register queue uses them) with 128-bit global loads of the thread's own points instead of
+// halo'd TMA boxes through the ring; 0: all planes through the ring (round-2 A/B:
+// profiles/ldgq_ab_r02.log, C2 -0.4..-1.4 %, C3 -0.7 %, C4 -0.5 %, bitwise identical)
+#ifndef RTM_LDGQ
+#define RTM_LDGQ 1
+#endif
+
 namespace rtm {
 
 // ------------------------------------------------------------------------------------
@@ -392,6 +400,9 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
     constexpr bool MQ = S::MQ;
     // queue slot of z offset k - 5 in unrolled iteration O
     constexpr auto QI = [](int O, int k) constexpr { return MQ ? (O + k) % 11 : O + k; };
+    // z-halo planes at the start of a unit that bypass the ring (consumer global loads); only
+    // in single-step launches, where the u buffer is read-only for the whole kernel
+    constexpr int QS = (RTM_LDGQ && !MS) ? 5 : 0;
     extern __shared__ __align__(128) float smem[];
     float* uring = smem;
     float* cring = smem + K * S::USLOT;
@@ -461,8 +472,8 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
                 const bool down = sweep_down(p, MS ? p.parity + k : p.parity, unit);
                 const int ub0 = (int)g.soff + (down ? g.ze + 9 : g.zs), ustep = down ? -1 : 1;
                 const int cz0 = down ? g.ze - 1 : g.zs;
-                auto put_u = [&](int j) {
-                    const uint32_t seq = gu + j, slot = seq % K;
+                auto put_u = [&](int j) {  // sweep position j >= QS
+                    const uint32_t seq = gu + j - QS, slot = seq % K;
                     if (seq >= K) mbar_wait(&empty_u[slot], ((seq / K) - 1) & 1);
                     mbar_expect_tx(&full_u[slot], S::UBYTES);
                     if (hint)
@@ -497,14 +508,14 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
                     asm volatile("griddepcontrol.wait;" ::: "memory");
                     waited = true;
                 }
-                for (int j = 0; j < 10; ++j) put_u(j);
+                for (int j = QS; j < 10; ++j) put_u(j);
                 for (int i = 0; i < n; ++i) {
                     if constexpr (D > 0) {
                         if (i >= ci) put_c(i);
                     }
                     put_u(i + 10);
                 }
-                gu += n + 10;
+                gu += n + 10 - QS;
                 gc += n;
             }
             if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -562,16 +573,28 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
                 if (lane == 0) mbar_arrive_u32(eu + 8 * slot);
             }
         };
+        if constexpr (QS > 0) {
+            // the unit's leading z-halo planes feed only this thread's z queue: 128-bit loads of
+            // its own 4 points, all in flight with the producer's first ring pass (the first
+            // output then waits for one memory round trip instead of two ring passes)
+            const float* ucol = p.u + col;
+            const long long ub0 = g.soff + (down ? g.ze + 9 : g.zs);
 #pragma unroll
-        for (int j = 0; j < 10; ++j) {
-            const uint32_t seq = gu + j;
+            for (int j = 0; j < QS; ++j)
+                q[j] = active ? __ldg(reinterpret_cast<const float4*>(ucol + (ub0 + (down ? -j : j)) * p.plane))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int j = QS; j < 10; ++j) {
+            const uint32_t seq = gu + j - QS;
             mbar_wait_u32(fu + 8 * (seq % K), (seq / K) & 1);
             q[j] = *reinterpret_cast<const float4*>(uown + (seq % K) * S::USLOT);
             if (j < 5) release_u(seq % K);
         }
         // running ring positions: plane gu+i+10 (new), gu+i+5 (current), u_prev/C gc+i
-        uint32_t sn = (gu + 10) % K, pn = ((gu + 10) / K) & 1;
-        uint32_t sc = (gu + 5) % K;
+        // (sweep positions; the ring sequence is QS behind)
+        uint32_t sn = (gu + 10 - QS) % K, pn = ((gu + 10 - QS) / K) & 1;
+        uint32_t sc = (gu + 5 - QS) % K;
         uint32_t sq = D > 0 ? gc % D : 0, pq = D > 0 ? (gc / D) & 1 : 0;
         float4 upv = make_float4(0.f, 0.f, 0.f, 0.f), cv = upv;
         if constexpr (D == 0) {
@@ -692,8 +715,8 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
             }
         }
 #pragma unroll 1
-        for (int j = n + 5; j < n + 10; ++j) release_u((gu + j) % K);  // planes used only by the queue
-        gu += n + 10;
+        for (int j = n + 5; j < n + 10; ++j) release_u((gu + j - QS) % K);  // planes used only by the queue
+        gu += n + 10 - QS;
         gc += n;
         if constexpr (MS) {
             // publish "unit done with step k": every consumer thread orders its own stores of the

@@ -2,7 +2,7 @@
 and step counts; every kernel variant must equal the naive kernel bitwise and the fp32 oracle
 within the one-step tolerance scaled by the step count (random z sweep direction, RTM_OPT_ZDIR);
 slab decompositions (halo modes 0-3, host-ordered or not, graphs or not) must equal the
-single-slab result bitwise.  Usage: python tools/fuzz_parity.py [cases] [seed]"""
+single-slab result bitwise.  Usage: python tests/fuzz_parity.py [cases] [seed]"""
 import sys
 import time
 from pathlib import Path

@@ -1067,13 +1067,13 @@ def test_bench_line_contract_and_consistency(P):
 
 
 def test_randomized_parity_fuzz_slice(P):
-    """40 cases of tools/fuzz_parity.py (random ragged shapes, velocities, ICs, sources, step
+    """40 cases of tests/fuzz_parity.py (random ragged shapes, velocities, ICs, sources, step
     counts): every variant bitwise equal to the naive kernel, slab modes bitwise equal to the
     single slab, the naive kernel within tolerance of the oracle."""
     import importlib.util
     import sys
     from pathlib import Path
-    path = Path(__file__).resolve().parent.parent / "tools" / "fuzz_parity.py"
+    path = Path(__file__).resolve().parent.parent / "tests" / "fuzz_parity.py"
     spec = importlib.util.spec_from_file_location("fuzz_parity", path)
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
