@@ -1,7 +1,8 @@
 """Small cases for compute-sanitizer (memcheck / racecheck / synccheck): every kernel family
-(naive, k_tiled, k_stream with and without the u_prev/C ring, the two-step k_tb2s, batched
-shots, slabs with copy, fused and flag-protocol halo modes, the asynchronous pipeline) on
-ragged grids of 16^3-64^3."""
+(naive, k_tiled, k_stream with and without the u_prev/C ring, U = 11, the two-row k_stream2,
+the cooperative multi-step and resident kernels, the two-step k_tb2s, batched shots, slabs
+with copy, fused, flag-protocol and pull halo modes, the asynchronous pipeline) on ragged grids
+of 16^3-64^3."""
 import sys
 from pathlib import Path
 
@@ -38,7 +39,9 @@ def run(shape, tile, steps=3, shots=1, devices=None, halo=0, tb_ctas=0):
 if __name__ == "__main__":
     names = {P.rtm_tile_name(i): i for i in range(P.rtm_num_tiles())}
     picks = ["naive", "tma64x16k10", "stream64x16k8d4u11", "stream64x14k10d5u4", "stream64x16k9d0u4",
-             "stream128x7k8d4u4"]
+             "stream128x7k8d4u4", "stream64x30k10d6u4", "stream64x30k10d6u11", "stream128x7k8d4u11",
+             "s2r64x28k10d6", "ms128x7k8d4u4", "ms64x30k10d6u11", "resident512x1"]
+    picks = [n for n in picks if n in names]
     for name in picks:
         run((21, 37, 68), names[name])
         run((16, 16, 16), names[name])
@@ -46,6 +49,7 @@ if __name__ == "__main__":
     run((40, 24, 32), None, devices=[0, 0])
     run((40, 24, 32), None, devices=[0, 0, 0], halo=1)
     run((40, 24, 32), None, devices=[0, 0, 0], halo=2)
+    run((40, 24, 32), None, devices=[0, 0, 0], halo=3)
     tb = [i for n, i in names.items() if n.startswith("tb2s_")][0]
     run((21, 37, 68), tb, steps=5)
     run((13, 61, 132), tb, steps=4, tb_ctas=6)       # several y-bands
