@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--share", type=int, default=0, help="RTM_OPT_SLAB_SHARE for --slabs > 1")
     ap.add_argument("--pdl", default="0", help="comma list of RTM_OPT_PDL values (interleaved)")
     ap.add_argument("--zdir", default="0", help="comma list of RTM_OPT_ZDIR values (interleaved)")
+    ap.add_argument("--l2persist", default="", help="comma list of cudaLimitPersistingL2CacheSize "
+                    "values in MB (interleaved; the L2 set-aside for evict_last / persisting lines)")
     args = ap.parse_args()
     import torch
     import paper_1310_8232_b200 as P
@@ -55,10 +57,17 @@ def main():
     tiles = [int(t) for t in args.tiles.split(",")] if args.tiles else list(range(P.rtm_num_tiles()))
     res = []
     for t in [t for _ in range(args.repeat) for t in tiles]:
-        for zc, cm, so, pdl, zd in [(int(z), c, int(o), int(q), int(d)) for z in args.zchunk.split(",")
-                                    for c in ([int(x, 0) for x in args.cache.split(",")] if args.cache else [None])
-                                    for o in args.shot_order.split(",") for q in args.pdl.split(",")
-                                    for d in args.zdir.split(",")]:
+        for zc, cm, so, pdl, zd, l2 in [(int(z), c, int(o), int(q), int(d), m)
+                                        for z in args.zchunk.split(",")
+                                        for c in ([int(x, 0) for x in args.cache.split(",")] if args.cache else [None])
+                                        for o in args.shot_order.split(",") for q in args.pdl.split(",")
+                                        for d in args.zdir.split(",")
+                                        for m in ([int(x) for x in args.l2persist.split(",")] if args.l2persist else [None])]:
+            if l2 is not None:
+                from cuda.bindings import runtime as crt
+                torch.cuda.synchronize()
+                err, = crt.cudaDeviceSetLimit(crt.cudaLimit.cudaLimitPersistingL2CacheSize, l2 << 20)
+                assert err == crt.cudaError_t.cudaSuccess, err
             P.rtm_set_option(h, P.RTM_OPT_SHOT_ORDER, so)
             P.rtm_set_option(h, P.RTM_OPT_PDL, pdl)
             P.rtm_set_option(h, P.RTM_OPT_ZDIR, zd)
@@ -80,7 +89,7 @@ def main():
                 ms = P.rtm_last_elapsed_ms(h) / args.ni
             gpts = cfg.points * args.shots / ms / 1e6
             r = {"tile": t, "name": P.rtm_tile_name(t), "zchunk": zc, "shot_order": so, "pdl": pdl,
-                 "zdir": zd,
+                 "zdir": zd, "l2persist_mb": l2,
                  "slabs": args.slabs, "halo": args.halo, "graphs": args.graphs, "share": args.share,
                  "enqueue_ms_per_step": round(P.rtm_last_enqueue_ms(h) / args.ni, 4),
                  "cache": hex(P.rtm_get_option(h, P.RTM_OPT_CACHE_MODE)), "ms_per_step": round(ms, 4),
@@ -89,7 +98,7 @@ def main():
             print(json.dumps(r), flush=True)
     agg = {}
     for r in res:
-        k = (r["tile"], r["zchunk"], r["cache"], r["shot_order"], r["pdl"], r["zdir"])
+        k = (r["tile"], r["zchunk"], r["cache"], r["shot_order"], r["pdl"], r["zdir"], r["l2persist_mb"])
         if k not in agg or r["ms_per_step"] < agg[k]["ms_per_step"]:
             agg[k] = r
     for r in sorted(agg.values(), key=lambda r: r["ms_per_step"]):
