@@ -112,9 +112,9 @@ struct Slab {
     unsigned long long* d_epoch = nullptr;     // pass epoch (never reset)
     unsigned* d_bar = nullptr;                 // k_resident grid barrier [2]
     cudaGraphExec_t tb_graph[4] = {nullptr, nullptr, nullptr, nullptr};  // key bank*2 + parity
-    unsigned long long* d_msflags = nullptr;   // multi-step launches: progress flag per (unit, consumer warp)
-    long long ms_units = 0;                    // capacity of d_msflags (flags)
-    unsigned long long ms_epoch = 0;           // per-launch tag (bits 40-63 of the flags)
+    unsigned long long* d_msflags = nullptr;   // multi-step launches: progress flag per work unit
+    long long ms_units = 0;                    // capacity of d_msflags
+    unsigned long long ms_epoch = 0;           // per-launch tag (upper 32 bits of the flags)
     int tb_graph_variant[4] = {-1, -1, -1, -1};
     // fused halo push with the flag protocol (halo mode 2): the neighbours' time-level buffers
     // and flag words — direct pointers in-process, CUDA-IPC mappings across processes
@@ -816,12 +816,9 @@ int step_resident(rtm_ctx* c, int nsteps) {
 }
 
 // Multi-step launches (kind 6): up to kMaxMsSteps time steps per cooperative launch of
-// k_stream<..., MS = true>; instead of a launch boundary between steps, each consumer warp
-// publishes its progress (flag = epoch << 40 | step << 20 | planes stored) and a unit's producer
-// checks, per plane, that the planes it loads were stored and the planes it will overwrite were
-// read by the neighbouring units (MsWaiter in rtm_kernels.cu).
-constexpr int kMaxMsSteps = (1 << 20) - 1;
-constexpr unsigned long long kMsEpochs = 1ull << 24;
+// k_stream<..., MS = true>; work units start a step once they and their face-neighbour units
+// have published the previous one (flags), instead of at a launch boundary.
+constexpr int kMaxMsSteps = 1 << 20;
 int step_mstep(rtm_ctx* c, int nsteps) {
     Slab& s = c->slabs[0];
     cudaStream_t st = s.stream();
@@ -839,24 +836,18 @@ int step_mstep(rtm_ctx* c, int nsteps) {
         p.tiles_y = (c->ny + tv.TY - 1) / tv.TY;
         p.r_chunks[0] = choose_chunks(c, s.occupancy, p.tiles_x * p.tiles_y * s.nshots, s.nzl);
         const long long units = (long long)p.tiles_x * p.tiles_y * p.r_chunks[0] * s.nshots;
-        const long long nflags = units * (tv.TX * tv.TY / 128);  // one per consumer warp
-        if (nflags > s.ms_units) {
+        if (units > s.ms_units) {
             if (s.d_msflags) {
                 CK(cudaStreamSynchronize(st));
                 CK(cudaFree(s.d_msflags));
                 s.d_msflags = nullptr;
             }
-            CK(cudaMalloc(&s.d_msflags, nflags * sizeof(unsigned long long)));
-            CK(cudaMemsetAsync(s.d_msflags, 0, nflags * sizeof(unsigned long long), st));
-            s.ms_units = nflags;
-            s.ms_epoch = 0;
-        }
-        if (s.ms_epoch + 1 >= kMsEpochs) {  // epochs wrap: clear the flags first
-            CK(cudaMemsetAsync(s.d_msflags, 0, s.ms_units * sizeof(unsigned long long), st));
-            s.ms_epoch = 0;
+            CK(cudaMalloc(&s.d_msflags, units * sizeof(unsigned long long)));
+            CK(cudaMemsetAsync(s.d_msflags, 0, units * sizeof(unsigned long long), st));
+            s.ms_units = units;
         }
         p.flags = s.d_msflags;
-        p.epoch = (++s.ms_epoch) << 40;  // flags of earlier launches are always smaller
+        p.epoch = (++s.ms_epoch) << 32;  // flags of earlier launches are always smaller
         p.nsteps = std::min(nsteps - k, kMaxMsSteps);
         p.step0 = (int)c->step;
         RET(prof_begin(c, st));

@@ -48,10 +48,8 @@ struct StencilParams {
     float* push_hi;
     // multi-step launches (kind 6, k_stream<..., MS = true>): nsteps time steps in ONE
     // cooperative launch, step k reading buf (parity + k) & 1 (u = k even ? u : next); the step
-    // index of step k is step0 + k; flags[unit * NW + w] = epoch | k << 20 | planes of step k
-    // stored by consumer warp w (epoch: a per-launch tag in bits 40-63); a unit's producer loads
-    // a plane of step k once the units that store it (and read what it overwrites) have
-    // published enough of step k - 1 (MsWaiter, rtm_kernels.cu)
+    // index of step k is step0 + k; a unit may start step k once it and its x/y/z neighbour
+    // units have published flags[unit] >= epoch | k (epoch: a per-launch tag in the upper 32 bits)
     int nsteps;
     int step0;
     unsigned long long epoch;

@@ -346,157 +346,50 @@ __device__ __forceinline__ int unit_index(const StencilParams& p, int shot, int 
     if (p.shot_major) return shot * ntiles * p.r_chunks[0] + chunk * ntiles + tile;
     return (chunk * ntiles + tile) * p.nshots + shot;
 }
-// ---- multi-step launches (MS): per-warp progress flags -----------------------------------
-// flags[unit * NW + w] = epoch | k << 20 | planes of step k that consumer warp w of the unit has
-// stored (published every kMsGrain planes and at the unit's end: the warp's gpu-scope fence,
-// then one release store).  A unit's sweep direction is its z-chunk's parity (odd chunks run
-// downward), the same in every step, so a unit's face neighbours (same chunk) sweep in step with
-// it and its z-neighbour chunks run the opposite way: every plane a unit reads at step k — its own
-// and its x/y neighbours' u^k at the same sweep position, the adjacent chunk's first planes at its
-// start, the other adjacent chunk's last planes at its end — was stored about one step-time
-// earlier, and every plane it overwrites (u^{k-1}) was read at least that long ago.  The
-// producer therefore checks, plane by plane, a progress target that is normally already met and
-// streams across step boundaries without draining the rings.
-#ifndef RTM_MS_GRAIN
-#define RTM_MS_GRAIN 16
-#endif
-constexpr int kMsGrain = RTM_MS_GRAIN;
-constexpr int kMsStepShift = 20;
-
-struct MsUnit {
-    int shot, chunk, tile;
-};
-__device__ __forceinline__ MsUnit ms_decode(const StencilParams& p, int unit) {
+// Spin (acquire, gpu scope) until flags[unit] and the flags of its face neighbours (x +- 1,
+// y +- 1 tiles of the same chunk; chunks +- 1 of the same tile; same shot) reach target, i.e.
+// until every unit whose u^{n+1} planes this unit's box reads has stored them (RAW) and has
+// finished reading the u^{n-1} planes this unit overwrites (WAR).  Then order the following
+// TMA (async-proxy) loads after the acquired generic-proxy stores.  4 s watchdog -> trap.
+__device__ __noinline__ void wait_unit_flags(const StencilParams& p, int unit, unsigned long long target) {
     const int ntiles = p.tiles_x * p.tiles_y;
-    MsUnit m;
-    int rest;
+    int shot, rest;
     if (p.shot_major) {
         const int per_shot = ntiles * p.r_chunks[0];
-        m.shot = unit / per_shot;
-        rest = unit - m.shot * per_shot;
+        shot = unit / per_shot;
+        rest = unit - shot * per_shot;
     } else {
-        m.shot = unit % p.nshots;
+        shot = unit % p.nshots;
         rest = unit / p.nshots;
     }
-    m.chunk = rest / ntiles;
-    m.tile = rest - m.chunk * ntiles;
-    return m;
-}
-__device__ __forceinline__ int ms_zb(const StencilParams& p, int c) {
-    return p.r_begin[0] + static_cast<int>((long long)c * p.r_len[0] / p.r_chunks[0]);
-}
-
-// The producer's view of its neighbours' progress in the previous step.  Slots: 0 = the unit
-// itself, 1-4 = the x-, x+, y-, y+ tiles of the same chunk (same z-range and direction, so their
-// planes align with this unit's sweep positions), 5 + (d + 5) = the chunk d away of the same
-// tile (|d| <= 5, only those intersecting the z-halo).  Per plane the check is one compare in
-// the common case; the 10 z-halo planes' owners and targets are computed once per unit-step.
-template <int NW>
-struct MsWaiter {
-    const StencilParams& p;
-    int n;
-    unsigned long long base;  // epoch | (k - 1) << 20: "planes of the previous step"
-    int wunit[16];
-    unsigned long long seen[16];
-    int hslot[10];            // z-halo sweep positions 0-4 and n+5 .. n+9: owner slot (-1: none)
-    unsigned long long htgt[10];
-    int safe_int;             // interior positions j <= safe_int are known to be ready
-#ifdef RTM_MS_DEBUG
-    unsigned long long* dbg_ns;
-    unsigned* dbg_n;
-#endif
-
-    __device__ MsWaiter(const StencilParams& p_, int unit, int k, const MsUnit& me, int zs, int ze, bool down)
-        : p(p_), n(ze - zs) {
-        base = p.epoch | ((unsigned long long)(k - 1) << kMsStepShift);
-        for (int i = 0; i < 16; ++i) wunit[i] = -1, seen[i] = 0;
-        const int ty = me.tile / p.tiles_x, tx = me.tile - ty * p.tiles_x;
-        wunit[0] = unit;
-        if (tx > 0) wunit[1] = unit_index(p, me.shot, me.chunk, me.tile - 1);
-        if (tx + 1 < p.tiles_x) wunit[2] = unit_index(p, me.shot, me.chunk, me.tile + 1);
-        if (ty > 0) wunit[3] = unit_index(p, me.shot, me.chunk, me.tile - p.tiles_x);
-        if (ty + 1 < p.tiles_y) wunit[4] = unit_index(p, me.shot, me.chunk, me.tile + p.tiles_x);
-        // chunk boundaries in 32-bit arithmetic (nzl * chunks < 2^31)
-        const int rb = p.r_begin[0], rl = p.r_len[0], rc = p.r_chunks[0];
-        auto zb = [&](int c) { return rb + (c * rl) / rc; };
-        for (int h = 0; h < 10; ++h) {
-            hslot[h] = -1;
-            htgt[h] = 0;
-            const int j = h < 5 ? h : n + h;  // sweep positions 0-4, n+5 .. n+9
-            const int z = down ? ze + RADIUS - 1 - j : zs - RADIUS + j;
-            if (z < rb || z >= rb + rl) continue;  // zero / external halo: static in this launch
-            int c2 = me.chunk + (z < zs ? -1 : 1);
-            while (zb(c2) > z) --c2;
-            while (zb(c2 + 1) <= z) ++c2;
-            const int pos = (c2 & 1) ? zb(c2 + 1) - 1 - z : z - zb(c2);  // odd chunks sweep down
-            const int slot = 10 + (c2 - me.chunk);
-            if (wunit[slot] < 0) wunit[slot] = unit_index(p, me.shot, c2, me.tile);
-            hslot[h] = slot;
-            htgt[h] = base | (unsigned long long)(pos + 1);
-        }
-        safe_int = RADIUS - 1;
-    }
-    __device__ __forceinline__ unsigned long long poll(int slot) const {
-        const unsigned long long* f = p.flags + (long long)wunit[slot] * NW;
-        unsigned long long mn = ~0ull;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            const unsigned long long v = ld_relaxed_gpu_u64(f + w);
-            mn = v < mn ? v : mn;
-        }
-        return mn;
-    }
-    __device__ void acquired() const {
-        fence_acq_rel_gpu();
-        fence_proxy_async_global();
-    }
-    // interior readiness from the face/own observations
-    __device__ __forceinline__ void update_safe() {
-        unsigned long long mn = ~0ull;
-#pragma unroll
-        for (int s = 0; s <= 4; ++s)
-            if (wunit[s] >= 0) mn = seen[s] < mn ? seen[s] : mn;
-        if (mn >= base + (1ull << kMsStepShift)) safe_int = 1 << 30;  // all in a later step
-        else if (mn >= base) safe_int = RADIUS - 1 + (int)(mn - base);
-        else safe_int = RADIUS - 1;
-    }
-    // one batch of relaxed polls of every neighbour (all loads in flight at once), then acquire
-    __device__ void refresh_all() {
-        unsigned long long v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = wunit[i] >= 0 ? poll(i) : 0;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) seen[i] = v[i] > seen[i] ? v[i] : seen[i];
-        update_safe();
-        acquired();
-    }
-    __device__ void spin_until(bool (MsWaiter::*ready)(int) const, int j) {
-        const unsigned long long t0 = globaltimer_ns();
+    const int chunk = rest / ntiles, tile = rest - chunk * ntiles;
+    const int ty = tile / p.tiles_x, tx = tile - ty * p.tiles_x;
+    // chunk c covers planes [zb(c), zb(c+1)); its u boxes read planes [zb(c) - 5, zb(c+1) + 5), so
+    // every chunk of the same tile that intersects that range is a z-neighbour (more than one on
+    // each side when chunks are shorter than the 5-plane halo)
+    auto zb = [&](int c2) {
+        return p.r_begin[0] + static_cast<int>((long long)c2 * p.r_len[0] / p.r_chunks[0]);
+    };
+    const int lo = zb(chunk) - RADIUS, hi = zb(chunk + 1) + RADIUS;
+    auto check = [&](int v, unsigned long long t0) {
+        const unsigned long long* f = p.flags + v;
+        if (ld_acquire_gpu_u64(f) >= target) return;
         unsigned spins = 0;
-        for (;;) {
-            refresh_all();
-            if ((this->*ready)(j)) break;
-            __nanosleep(32);
+        while (ld_acquire_gpu_u64(f) < target) {
+            __nanosleep(64);
             if ((++spins & 255) == 0 && globaltimer_ns() - t0 > kWatchdogNs) __trap();
         }
-#ifdef RTM_MS_DEBUG
-        dbg_ns[1] += globaltimer_ns() - t0;
-        dbg_n[1] += 1;
-#endif
-    }
-    __device__ bool ready(int j) const {
-        if (j >= RADIUS && j < n + RADIUS) return j <= safe_int;
-        const int h = j < RADIUS ? j : j - n;
-        return hslot[h] < 0 || seen[hslot[h]] >= htgt[h];
-    }
-    // the box plane at sweep position j (0 .. n + 9): every store it depends on and every read of
-    // the plane it will later overwrite are done (RAW and WAR, see above)
-    __device__ __forceinline__ void before_box(int j) {
-        if (j >= RADIUS && j < n + RADIUS && j <= safe_int) return;  // the common case
-        if (ready(j)) return;
-        spin_until(&MsWaiter::ready, j);
-    }
-};
+    };
+    const unsigned long long t0 = globaltimer_ns();
+    check(unit, t0);
+    if (tx > 0) check(unit_index(p, shot, chunk, tile - 1), t0);
+    if (tx + 1 < p.tiles_x) check(unit_index(p, shot, chunk, tile + 1), t0);
+    if (ty > 0) check(unit_index(p, shot, chunk, tile - p.tiles_x), t0);
+    if (ty + 1 < p.tiles_y) check(unit_index(p, shot, chunk, tile + p.tiles_x), t0);
+    for (int c2 = chunk - 1; c2 >= 0 && zb(c2 + 1) > lo; --c2) check(unit_index(p, shot, c2, tile), t0);
+    for (int c2 = chunk + 1; c2 < p.r_chunks[0] && zb(c2) < hi; ++c2) check(unit_index(p, shot, c2, tile), t0);
+    fence_proxy_async_global();
+}
 
 template <int TX, int TY, int K, int D, int MINB, int U, bool MS>
 __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
@@ -564,46 +457,24 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
             const uint64_t cpol = policy_evict_first();
             uint32_t gu = 0, gc = 0;
             bool waited = false;  // griddepcontrol.wait done (see above)
-#ifdef RTM_MS_DEBUG
-            unsigned long long dns[16] = {};
-            unsigned dn[16] = {};
-            const unsigned long long tk0 = globaltimer_ns();
-#endif
             for (int k = 0; k < nst; ++k)
             for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
                 const CUtensorMap* tmu = (MS && (k & 1)) ? &tm_u2 : &tm_u;
                 const CUtensorMap* tmp = (MS && (k & 1)) ? &tm_up2 : &tm_up;
+                if constexpr (MS) {
+                    if (k > 0) wait_unit_flags(p, unit, p.epoch | (unsigned long long)k);
+                }
                 const UnitGeom g = unit_geom(p, unit, TX, TY);
                 const int n = g.ze - g.zs;
                 // z sweep direction of this step (RTM_OPT_ZDIR): down on odd-parity steps, so a
                 // step starts on the planes the previous step touched last (still in L2).
                 // Buffer plane of sweep position j of the u box / of output i (u_prev tile):
-                const MsUnit mu = ms_decode(p, unit);
-                const bool down = MS ? (mu.chunk & 1) != 0 : sweep_down(p, p.parity, unit);
-                // MS, k > 0: per-plane progress checks against the previous step (see MsWaiter)
-                MsWaiter<S::NW> msw(p, unit, k, mu, g.zs, g.ze, down);
-#ifdef RTM_MS_DEBUG
-                msw.dbg_ns = dns;
-                msw.dbg_n = dn;
-#endif
-#if !defined(RTM_MS_NOWAIT) && !defined(RTM_MS_NOREFRESH)
-                if (MS && k > 0) msw.refresh_all();
-#endif
+                const bool down = sweep_down(p, MS ? p.parity + k : p.parity, unit);
                 const int ub0 = (int)g.soff + (down ? g.ze + 9 : g.zs), ustep = down ? -1 : 1;
                 const int cz0 = down ? g.ze - 1 : g.zs;
                 auto put_u = [&](int j) {  // sweep position j >= QS
                     const uint32_t seq = gu + j - QS, slot = seq % K;
                     if (seq >= K) mbar_wait(&empty_u[slot], ((seq / K) - 1) & 1);
-#ifndef RTM_MS_NOWAIT
-#ifdef RTM_MS_DEBUG
-                    const unsigned long long tb0 = globaltimer_ns();
-#endif
-                    if (MS && k > 0) msw.before_box(j);
-#ifdef RTM_MS_DEBUG
-                    dns[0] += globaltimer_ns() - tb0;
-                    ++dn[0];
-#endif
-#endif
                     mbar_expect_tx(&full_u[slot], S::UBYTES);
                     if (hint)
                         tma_load_3d_hint(uring + slot * S::USLOT, tmu, g.x0 - 8, g.y0 - 5,
@@ -648,14 +519,6 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
                 gc += n;
             }
             if (!waited) asm volatile("griddepcontrol.wait;" ::: "memory");
-#ifdef RTM_MS_DEBUG
-            if (MS && (blockIdx.x % 37) == 0) {
-                printf("MSDBG cta %d t_kernel_us %.1f", (int)blockIdx.x, (globaltimer_ns() - tk0) * 1e-3);
-                for (int i = 0; i < 16; ++i)
-                    if (dn[i]) printf(" | s%d n=%u us=%.1f", i, dn[i], dns[i] * 1e-3);
-                printf("\n");
-            }
-#endif
         }
         return;
     }
@@ -694,7 +557,7 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
         // sweep direction (see the producer); the z register queue is filled in sweep order, so
         // a downward sweep mirrors it — the z pair sums u(z-m) + u(z+m) are commutative (IEEE
         // addition), so results are bitwise those of the upward sweep
-        const bool down = MS ? (ms_decode(p, unit).chunk & 1) != 0 : sweep_down(p, p.parity, unit);
+        const bool down = sweep_down(p, MS ? p.parity + k : p.parity, unit);
         const int z0 = down ? g.ze - 1 : g.zs, zstep = down ? -1 : 1;
         const long long pstep = down ? -p.plane : p.plane;
         float* outp = nextbuf + (g.soff + z0 + 5) * p.plane + col;  // also u_prev (D == 0)
@@ -831,17 +694,6 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
                 st_mode4(outp, o4, plain);
                 if (p.push_lo || p.push_hi) push_halo4(p, z0 + zstep * it, col, o4);
             }
-            if constexpr (MS) {  // progress of this warp: its stores ordered at gpu scope, then released
-                if ((it + 1) % kMsGrain == 0 || it + 1 == n) {
-#ifndef RTM_MS_NOFENCE
-                    __threadfence();
-#endif
-                    __syncwarp();
-                    if (lane == 0)
-                        st_release_gpu_u64(p.flags + (long long)unit * S::NW + warp,
-                                           p.epoch | ((unsigned long long)k << kMsStepShift) | (unsigned)(it + 1));
-                }
-            }
             if (++sn == K) sn = 0, pn ^= 1;
             if (++sc == K) sc = 0;
             if constexpr (D > 0) {
@@ -866,6 +718,14 @@ __global__ void __launch_bounds__(StreamShape<TX, TY, K, D, U>::NT, MINB)
         for (int j = n + 5; j < n + 10; ++j) release_u((gu + j - QS) % K);  // planes used only by the queue
         gu += n + 10 - QS;
         gc += n;
+        if constexpr (MS) {
+            // publish "unit done with step k": every consumer thread orders its own stores of the
+            // unit at gpu scope (fence), the CTA barrier collects them, one gpu-scope release is
+            // read by the neighbours' producers (acquire + async-proxy fence before their TMA)
+            __threadfence();
+            asm volatile("bar.sync 1, %0;" ::"n"(S::NW * 32) : "memory");
+            if (tid == 0) st_release_gpu_u64(p.flags + unit, p.epoch | (unsigned long long)(k + 1));
+        }
     }
 }
 
