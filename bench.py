@@ -64,6 +64,9 @@ def parse():
                          "ranks may share a GPU (then host-ordered) - exercises the N > 1 bench "
                          "path on one GPU, not a scaling measurement")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-verify", action="store_true",
+                    help="N > 1: skip the untimed slab-by-slab bitwise check against a "
+                         "single-GPU context on rank 0")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="short run for ncu captures (no extras)")
     return ap.parse_args()
@@ -256,6 +259,60 @@ def cpu_baseline(cfg, v_full):
 
 
 # ------------------------------------------------------------------------------ b200 arm
+def field_sums(t, planes_per_chunk=64):
+    """Two 64-bit sums of the fp32 bit patterns of a (nz, ny, nx) field: plain and
+    position-weighted (weight = flat index mod 1021 + 1), so equal sums mean equal bits up to a
+    collision, and a shifted or transposed plane changes the weighted sum.  Chunked over planes
+    to bound the int64 temporaries."""
+    import torch
+    s1 = s2 = 0
+    plane = t.shape[-1] * t.shape[-2]
+    for z in range(0, t.shape[0], planes_per_chunk):
+        b = t[z:z + planes_per_chunk].reshape(-1).view(torch.int32).to(torch.int64)
+        w = torch.arange(z * plane, z * plane + b.numel(), device=t.device, dtype=torch.int64) % 1021 + 1
+        s1 += int(b.sum().item())
+        s2 += int((b * w).sum().item())
+        del b, w
+    return s1, s2
+
+
+def verify_slabs(args, P, ri, cfg, v_full, nsteps, d_out, z0, nzl, rank, world, dev, tdist, barrier):
+    """Slab-by-slab bitwise check of the distributed result (u^N of the last bench step, in
+    d_out) against a single-GPU context of the whole grid run by rank 0 with the same velocity,
+    sources and time steps.  Returns the record rank 0 adds to the JSON line (None elsewhere)."""
+    import torch
+    mine = (z0, nzl) + field_sums(d_out[0])
+    got = [None] * world
+    tdist.all_gather_object(got, mine)
+    if rank != 0:
+        barrier()
+        return None
+    t0 = time.perf_counter()
+    h1 = P.rtm_create(cfg.nx, cfg.ny, cfg.nz, cfg.dx, cfg.dt, ri.COEFFS_F32)
+    try:
+        P.rtm_set_velocity(h1, np.ascontiguousarray(v_full))
+        for (x, y, z, w) in cfg.sources(v_full):
+            P.rtm_inject_source(h1, x, y, z, w[:nsteps] if len(w) > nsteps else w)
+        P.rtm_step(h1, nsteps)
+        full = torch.empty((cfg.nz, cfg.ny, cfg.nx), dtype=torch.float32, device=dev)
+        P.rtm_read_field_device(h1, full.data_ptr())
+        torch.cuda.synchronize(dev)
+        bad = []
+        for r, (zr, nr, s1, s2) in enumerate(got):
+            if field_sums(full[zr:zr + nr]) != (s1, s2):
+                bad.append(r)
+        finite = bool(torch.isfinite(full).all().item())
+        del full
+    finally:
+        P.rtm_destroy(h1)
+    barrier()
+    return {"reference": "single-GPU context of the whole grid on rank 0 (rtm_create, same "
+                         "velocity, sources and time steps, default variant)",
+            "time_steps": nsteps, "slabs": world, "bitwise": not bad and finite,
+            "mismatched_ranks": bad, "method": "per-slab sums of the fp32 bit patterns "
+            "(plain and position-weighted)", "seconds": round(time.perf_counter() - t0, 2)}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -479,6 +536,14 @@ def main():
         e2e["matches_device_result"] = bool(np.array_equal(hout_np[(args.steps - 1) % 2],
                                                            d_out.cpu().numpy()))
 
+    # N > 1: the distributed result checked against ONE single-GPU context of the whole grid
+    # (same inputs, same time steps) on rank 0 — bitwise, slab by slab (every slab
+    # decomposition is bitwise equal to G = 1).  Untimed; makes every scaling line self-validating.
+    slab_parity = None
+    if world > 1 and not args.no_verify and not args.ncu:
+        slab_parity = verify_slabs(args, P, ri, cfg, v_full, nsteps, d_out, z0, nzl, rank, world,
+                                   dev, tdist, barrier)
+
     cpu = None
     if rank == 0 and not args.no_cpu and not args.ncu:
         cpu = cpu_baseline(cfg, v_full)
@@ -520,6 +585,8 @@ def main():
             "autotune": tune,
             "cpu_baseline": cpu, "finite": finite,
         }
+        if slab_parity is not None:
+            line["slab_parity"] = slab_parity
         if args.peer:
             line["test_mode"] = (f"peer contexts over gloo, {world} ranks on {min(ndev, world)} GPU(s)"
                                  + (", host-ordered: not a scaling measurement" if shared else ""))

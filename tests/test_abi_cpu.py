@@ -244,3 +244,29 @@ def test_c_example_builds_against_the_header_and_library(P, tmp_path):
         pytest.skip("GPU present (tests/test_gpu_round2.py runs it)")
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
     assert r.returncode == 1 and "no CUDA device" in r.stderr
+
+
+def test_bench_slab_parity_sums_detect_changes():
+    """bench.py's N > 1 self-check (`slab_parity`) compares two 64-bit sums of the fp32 bit
+    patterns per slab: one flipped bit, a sign change of a zero, or two swapped planes must all
+    change them; a bitwise-equal copy must not."""
+    import importlib.util
+    import torch
+    spec = importlib.util.spec_from_file_location("bench_mod", ROOT / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    g = torch.Generator().manual_seed(5)
+    t = torch.randn((7, 5, 12), generator=g, dtype=torch.float32)
+    t[3, 2, 4] = 0.0
+    ref = bench.field_sums(t, planes_per_chunk=2)
+    assert bench.field_sums(t.clone(), planes_per_chunk=3) == ref  # chunking does not matter
+    a = t.clone()
+    a.view(torch.int32)[1, 1, 1] ^= 1  # one ulp
+    assert bench.field_sums(a) != ref
+    b = t.clone()
+    b[3, 2, 4] = -0.0  # equal as floats, different bits
+    assert bench.field_sums(b) != ref
+    c = t.clone()
+    c[[2, 5]] = t[[5, 2]]  # two planes swapped: same plain sum, different weighted sum
+    s1, s2 = bench.field_sums(c)
+    assert s1 == ref[0] and s2 != ref[1]

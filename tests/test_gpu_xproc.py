@@ -106,3 +106,6 @@ def test_bench_n2_path_with_peer_contexts_on_one_gpu():
     assert d["n_gpus"] == 2 and d["value"] > 0 and "test_mode" in d and d["finite"] is True
     assert d["config"]["parallelism"] == "z-slab x2" and d["config"]["halo"] == "IPC copy-engine pull"
     assert d["e2e"]["value"] > 0 and d["e2e"]["matches_device_result"] is True
+    # the untimed slab-by-slab check against one single-GPU context of the whole grid
+    sp = d["slab_parity"]
+    assert sp["bitwise"] is True and sp["slabs"] == 2 and sp["mismatched_ranks"] == []
