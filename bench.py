@@ -46,6 +46,9 @@ def parse():
                     help="kernel variant; -1 = choose with rtm_autotune (untimed, before warm-up)")
     ap.add_argument("--tune-ni", type=int, default=12,
                     help="autotune iterations per candidate (raised automatically on small grids)")
+    ap.add_argument("--tune-refine", type=int, default=4,
+                    help="re-time the N fastest tuner candidates in 3 interleaved rounds of 3 nI "
+                         "steps and keep the lowest mean (power-cap drift, DESIGN.md §5); <= 1: off")
     ap.add_argument("--lattice", type=int, default=0,
                     help="P > 1: autotune over the stream tiles x the paper's P-parts z-chunk "
                          "lattice (PAPER.md:296-301); 0: automatic z-chunk per tile")
@@ -276,6 +279,37 @@ def field_sums(t, planes_per_chunk=64):
     return s1, s2
 
 
+def refine_selection(P, h, nI, cands, zcs, times, top, rounds=3):
+    """Second tuner pass over the `top` fastest (tile, z-chunk) candidates of the selection
+    phase: `rounds` interleaved rounds of 3 nI steps each (one rtm_autotune call whose candidate
+    list repeats the finalists), keeping the lowest MEAN time.  A single nI-step window per
+    candidate ranks variants 1-2 % apart by the clock they happened to get: under the board's
+    power cap the SM clock drifts during the tuner, so the candidates timed later run slower
+    (DESIGN.md §5).  Times are max over ranks (library), so every rank picks the same."""
+    zcs = list(zcs) if zcs is not None else [0] * len(cands)
+    order = sorted((t, k) for k, t in enumerate(times) if np.isfinite(t))
+    fin = []
+    for _, k in order:
+        if (cands[k], zcs[k]) not in fin:
+            fin.append((cands[k], zcs[k]))
+        if len(fin) == top:
+            break
+    if len(fin) < 2:
+        return {"finalists": len(fin), "selected": P.rtm_tile_name(fin[0][0]) if fin else None,
+                "zchunk": fin[0][1] if fin else None}
+    t2 = [t for _ in range(rounds) for t, _ in fin]
+    z2 = [z for _ in range(rounds) for _, z in fin]
+    _, tt = P.rtm_autotune(h, 3 * nI, tiles=t2, zchunks=z2)
+    mean = [float(np.mean(tt[j::len(fin)])) for j in range(len(fin))]
+    best = int(np.argmin(mean))
+    P.rtm_set_tile(h, fin[best][0])
+    P.rtm_set_zchunk(h, fin[best][1])
+    return {"finalists": len(fin), "rounds": rounds, "nI": 3 * nI,
+            "mean_ms_per_step": {f"{P.rtm_tile_name(t)}/z{z}": round(m / (3 * nI), 5)
+                                 for (t, z), m in zip(fin, mean)},
+            "selected": P.rtm_tile_name(fin[best][0]), "zchunk": fin[best][1]}
+
+
 def verify_slabs(args, P, ri, cfg, v_full, nsteps, d_out, z0, nzl, rank, world, dev, tdist, barrier):
     """Slab-by-slab bitwise check of the distributed result (u^N of the last bench step, in
     d_out) against a single-GPU context of the whole grid run by rank 0 with the same velocity,
@@ -403,6 +437,10 @@ def main():
                 "zchunk": res.get("best_zchunk"), "lattice_P": args.lattice or None,
                 "actual_time_ms": round(res["actual_time_ms"], 4),
                 "quality_pct": round(res["quality_pct"], 2)}
+        if args.tune_refine > 1:
+            tune["refine"] = refine_selection(P, h, nI, cands, zcs, times, args.tune_refine)
+            tune["selected"] = tune["refine"]["selected"]
+            tune["zchunk"] = tune["refine"]["zchunk"]
 
     def barrier():
         if world > 1:
