@@ -1064,6 +1064,12 @@ def test_bench_line_contract_and_consistency(P):
     assert d["e2e"]["h2d_bytes_per_step"] == nbytes and d["e2e"]["d2h_bytes_per_step"] == nbytes
     assert d["e2e"]["value"] > 0 and d["e2e"]["matches_device_result"] is True
     assert d["config"]["workload"] == "C1" and d["clocks"]["sm_max_mhz"]
+    # the tuner refinement installed its pick: the timed kernel is the refined selection
+    ref = d["autotune"]["refine"]
+    assert ref["selected"] == d["autotune"]["selected"]
+    if ref["finalists"] > 1:
+        assert len(ref["mean_ms_per_step"]) == ref["finalists"]
+        assert d["kernel_variant"] == ref["selected"] or ref["selected"] in rf["kernel"]
 
 
 def test_randomized_parity_fuzz_slice(P):
