@@ -46,9 +46,9 @@ def parse():
                     help="kernel variant; -1 = choose with rtm_autotune (untimed, before warm-up)")
     ap.add_argument("--tune-ni", type=int, default=12,
                     help="autotune iterations per candidate (raised automatically on small grids)")
-    ap.add_argument("--tune-refine", type=int, default=4,
-                    help="re-time the N fastest tuner candidates in 3 interleaved rounds of 3 nI "
-                         "steps and keep the lowest mean (power-cap drift, DESIGN.md §5); <= 1: off")
+    ap.add_argument("--tune-refine", type=int, default=6,
+                    help="re-time the N fastest tuner candidates in 3 interleaved rounds of >= 100 ms "
+                         "windows and keep the lowest mean (power-cap drift, DESIGN.md §7); <= 1: off")
     ap.add_argument("--lattice", type=int, default=0,
                     help="P > 1: autotune over the stream tiles x the paper's P-parts z-chunk "
                          "lattice (PAPER.md:296-301); 0: automatic z-chunk per tile")
@@ -279,13 +279,14 @@ def field_sums(t, planes_per_chunk=64):
     return s1, s2
 
 
-def refine_selection(P, h, nI, cands, zcs, times, top, rounds=3):
+def refine_selection(P, h, nI, cands, zcs, times, top, rounds=3, window_ms=100.0):
     """Second tuner pass over the `top` fastest (tile, z-chunk) candidates of the selection
     phase: `rounds` interleaved rounds of 3 nI steps each (one rtm_autotune call whose candidate
     list repeats the finalists), keeping the lowest MEAN time.  A single nI-step window per
     candidate ranks variants 1-2 % apart by the clock they happened to get: under the board's
-    power cap the SM clock drifts during the tuner, so the candidates timed later run slower
-    (DESIGN.md §5).  Times are max over ranks (library), so every rank picks the same."""
+    power cap the SM clock drifts during the tuner, so the candidates timed later run slower,
+    and short windows favour variants that only win at full clock.  Each
+    refinement window runs max(3 nI, ~window_ms) steps.  Times are max over ranks (library), so every rank picks the same."""
     zcs = list(zcs) if zcs is not None else [0] * len(cands)
     order = sorted((t, k) for k, t in enumerate(times) if np.isfinite(t))
     fin = []
@@ -299,13 +300,16 @@ def refine_selection(P, h, nI, cands, zcs, times, top, rounds=3):
                 "zchunk": fin[0][1] if fin else None}
     t2 = [t for _ in range(rounds) for t, _ in fin]
     z2 = [z for _ in range(rounds) for _, z in fin]
-    _, tt = P.rtm_autotune(h, 3 * nI, tiles=t2, zchunks=z2)
+    # windows of >= ~100 ms (the bench step is sustained load; C3's 29-step selection windows
+    # are 10 ms), at least 3 nI steps
+    nI2 = int(min(20000, max(3 * nI, np.ceil(window_ms / (order[0][0] / nI)))))
+    _, tt = P.rtm_autotune(h, nI2, tiles=t2, zchunks=z2)
     mean = [float(np.mean(tt[j::len(fin)])) for j in range(len(fin))]
     best = int(np.argmin(mean))
     P.rtm_set_tile(h, fin[best][0])
     P.rtm_set_zchunk(h, fin[best][1])
-    return {"finalists": len(fin), "rounds": rounds, "nI": 3 * nI,
-            "mean_ms_per_step": {f"{P.rtm_tile_name(t)}/z{z}": round(m / (3 * nI), 5)
+    return {"finalists": len(fin), "rounds": rounds, "nI": nI2,
+            "mean_ms_per_step": {f"{P.rtm_tile_name(t)}/z{z}": round(m / nI2, 5)
                                  for (t, z), m in zip(fin, mean)},
             "selected": P.rtm_tile_name(fin[best][0]), "zchunk": fin[best][1]}
 

@@ -54,7 +54,7 @@ def test_refine_picks_lowest_mean_not_lowest_window():
     fake = FakeLib({35: [99.0, 99.0, 99.0], 48: [98.0, 101.0, 101.0], 49: [102.0, 102.0, 102.0]})
     r = b.refine_selection(fake, None, 12, cands, zcs, times, top=3)
     nI, t2, z2 = fake.calls[0]
-    assert nI == 36
+    assert nI == 37                                   # >= 100 ms windows: ceil(100 / (32.6 / 12))
     assert t2 == [48, 35, 49] * 3 and z2 == [0] * 9      # distinct finalists, interleaved rounds
     assert r["selected"] == "t35" and fake.tile == 35 and fake.zchunk == 0
     assert r["mean_ms_per_step"]["t48/z0"] > r["mean_ms_per_step"]["t35/z0"]
@@ -67,9 +67,17 @@ def test_refine_distinguishes_zchunks_and_skips_nan():
     times = np.array([10.0, 11.0, np.nan, 12.0])
     fake = FakeLib({35: [5.0, 9.0, 5.0, 9.0, 5.0, 9.0], 49: [1.0, 1.0, 1.0]})
     r = b.refine_selection(fake, None, 4, cands, zcs, times, top=2)
-    _, t2, z2 = fake.calls[0]
+    nI, t2, z2 = fake.calls[0]
+    assert nI == 40 and r["nI"] == 40                 # ceil(100 ms / 2.5 ms)
     assert t2 == [35, 35] * 3 and z2 == [0, 64] * 3       # NaN (failed) candidate never a finalist
     assert fake.tile == 35 and fake.zchunk == 0 and r["zchunk"] == 0
+
+
+def test_refine_window_at_least_three_selection_windows():
+    b = _bench()
+    fake = FakeLib({1: [1.0] * 3, 2: [2.0] * 3})
+    b.refine_selection(fake, None, 50, [1, 2], None, np.array([500.0, 600.0]), top=2)
+    assert fake.calls[0][0] == 150                    # 3 nI when nI steps already exceed 100 ms
 
 
 def test_refine_single_finalist_makes_no_call():
